@@ -1,0 +1,349 @@
+"""Benchmark: nnz-split SpMM (Appendix A.4 schedule, N=128) on the BASELINE
+cfg2 matrix -- R-MAT scale 20 (1,048,576^2), 50M nnz, fp32 -- the config
+BASELINE.json's north star quotes its target on.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One JSON line on rank 0.  `value` = whole-job GFLOP/s (2*nnz*N / t) with
+operands resident in HBM, t = mean CUDA-event time of one spx_launch
+(spmm_nnz_kernel + carry fix-up) after an L2 flush, max over ranks.
+`e2e` = the same metric through the public API (`interpret`) with pinned
+host inputs: H2D of A and B, the launch and the D2H of C inside the timed
+region.  `roofline` compares compulsory bytes per launch
+with the measured HBM copy bandwidth.  `cpu_baseline` times the CPU oracle
+(oracle/spx_oracle.c, OpenMP, all host threads) on a bounded row sample.
+
+N>1 (torchrun): rows are partitioned nnz-balanced (spx_partition); each
+rank times its shard's kernel (sharded-output throughput);
+the C gather (NCCL all-gather) is timed and reported separately.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "SpMM/SpMV GFLOP/s and % HBM roofline at 1/2/4/8 B200 vs CPU oracle"
+WORKLOAD = "cfg2: CSR SpMM nnz-split (A.4: pos+fuse+split), R-MAT scale 20, 1048576^2, 50M nnz x dense N=128, fp32"
+FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--nnz", type=int, default=50_000_000)
+    ap.add_argument("--ncols", type=int, default=128)
+    ap.add_argument("--tb", type=int, default=2048, help="NNZ_PER_TB")
+    ap.add_argument("--warp", type=int, default=256, help="NNZ_PER_WARP")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-flush", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            d = json.loads(p.read_text())
+            return float(d["hbm_gbs"]), "measured"
+        except Exception:
+            pass
+    return FALLBACK_HBM_GBS, "fallback"
+
+
+def compulsory_bytes(M, K, N, nnz, es=4):
+    # 8*nnz + 4(M+1) + 4*K*N + 4*M*N  (crd+vals, pos, B, C)
+    return (4 + es) * nnz + 4 * (M + 1) + es * K * N + es * M * N
+
+
+def load_traffic():
+    p = ROOT / "profiles" / "spmm_traffic.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text()).get("dram_bytes_per_launch")
+        except Exception:
+            return None
+    return None
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the measured region (B200_PROFILING.md)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in out.strip().splitlines():
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline(A, B, nnz_sample: int):
+    """Oracle SpMM (fp64 accumulation, OpenMP over all host threads) on the
+    leading rows holding ~nnz_sample nonzeros."""
+    from oracle import oracle as O
+
+    r1 = int(np.searchsorted(A.pos, min(nnz_sample, A.nnz), side="left"))
+    r1 = max(1, min(r1, A.M))
+    nnz_s = int(A.pos[r1])
+    O.spmm(A.pos, A.crd, A.vals32, B, rows=(0, min(r1, 1024)))  # warm
+    t0 = time.perf_counter()
+    O.spmm(A.pos, A.crd, A.vals32, B, rows=(0, r1))
+    dt = time.perf_counter() - t0
+    flops = 2.0 * nnz_s * B.shape[1]
+    return {"value": round(flops / dt / 1e9, 3), "unit": "GFLOP/s", "cores": O.threads(), "kind": "port",
+            "sample": f"rows [0,{r1}) of cfg2 = {nnz_s} of {A.nnz} nnz, N={B.shape[1]}, one pass, {dt:.2f} s"}
+
+
+def host_cpu_info():
+    try:
+        model = next(ln.split(":", 1)[1].strip() for ln in open("/proc/cpuinfo") if ln.startswith("model name"))
+    except Exception:
+        model = "unknown"
+    return model
+
+
+def workload(args):
+    from paper_2001_00532_b200 import synth
+
+    A = synth.rmat_csr(20, args.nnz, seed=2)
+    A.vals32 = A.vals.astype(np.float32)
+    B = synth.dense((A.N, args.ncols), seed=202, dtype=np.float32)
+    return A, B
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import torch  # noqa: F401  (same interpreter; nothing on the GPU)
+
+    A, B = workload(args)
+    from oracle import oracle as O
+
+    sample = min(A.nnz, 5_000_000)
+    vals = []
+    for _ in range(args.warmup):
+        cpu_baseline(A, B, min(sample, 500_000))
+    for _ in range(args.steps):
+        vals.append(cpu_baseline(A, B, sample)["value"])
+    v = statistics.median(vals)
+    cb = cpu_baseline(A, B, sample)
+    cb["value"] = v
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "GFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": WORKLOAD + " -- CPU oracle port (the reference ships no executable SpMM)",
+                   "nnz": A.nnz, "N": args.ncols, "host_cpu": host_cpu_info()},
+        "ms_per_step": round(2.0 * sample * args.ncols / (v * 1e9) * 1e3, 3),
+        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2001_00532_b200 import _lib, corpus, lower
+    from paper_2001_00532_b200.execution import Executor, interpret
+    from paper_2001_00532_b200.formats import DeviceTensor
+    from paper_2001_00532_b200.partition import csr_shards, gather_rows
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    A, B = workload(args)
+    N = args.ncols
+    bound = math.ceil(N / 32)
+    prog = lower(corpus.build("A4", NNZ_PER_TB=args.tb, NNZ_PER_WARP=args.warp, BOUND=bound))
+
+    if world > 1:
+        shard = csr_shards(A.pos, A.crd, A.vals32, world)[rank]
+        pos, crd, vals, rows = shard.pos, shard.crd, shard.vals, shard.row1 - shard.row0
+    else:
+        pos, crd, vals, rows = A.pos, A.crd, A.vals32, A.M
+    nnz_local = len(crd)
+    Ad = DeviceTensor.from_arrays((rows, A.N), "ds", {1: pos}, {1: crd}, vals, device=dev, dtype="f32")
+    Bd = DeviceTensor.dense(B, device=dev, dtype="f32")
+    out = torch.empty(rows * N, dtype=torch.float32, device=dev)
+    ex = Executor(prog, {"A": Ad, "B": Bd}, out, dtype="f32")
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+
+    for _ in range(args.warmup):
+        ex.launch()
+    torch.cuda.synchronize(dev)
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    # keep the GPU busy ~1 s so the clock sampler sees the loaded state
+    t_end = time.perf_counter() + 1.0
+    while time.perf_counter() < t_end:
+        for _ in range(20):
+            ex.launch()
+        torch.cuda.synchronize(dev)
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    l0 = _lib.launch_count()
+    for k in range(args.steps):
+        if not args.no_flush:
+            flush.zero_()
+        starts[k].record(stream)
+        ex.launch(stream.cuda_stream)
+        ends[k].record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    launches = _lib.launch_count() - l0
+    clocks = sampler.stop()
+    times = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    t_ms = statistics.mean(times)
+    if world > 1:
+        tt = torch.tensor([t_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+
+    nnz_total = A.nnz
+    flops = 2.0 * nnz_total * N
+    value = flops / (t_ms * 1e-3) / 1e9
+
+    # roofline (compulsory bytes of this rank's launch / its duration)
+    hbm, peak_kind = peaks()
+    cb_local = compulsory_bytes(rows, A.N, N, nnz_local)
+    achieved = cb_local / (statistics.mean(times) * 1e-3) / 1e9
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+            "frac": round(achieved / hbm, 4), "traffic": load_traffic(), "peak_kind": peak_kind,
+            "kernel": "spmm_nnz_kernel + carry_fixup_kernel (one spx_launch)",
+            "algorithmic_bytes_per_launch": cb_local}
+
+    # gather of the sharded output (reported separately)
+    gather_ms = None
+    if world > 1:
+        counts = [0] * world
+        shards = csr_shards(A.pos, A.crd, A.vals32, world)
+        counts = [s.row1 - s.row0 for s in shards]
+        torch.cuda.synchronize(dev)
+        dist.barrier()
+        g0 = time.perf_counter()
+        full = gather_rows(out.view(rows, N), counts)
+        torch.cuda.synchronize(dev)
+        gather_ms = (time.perf_counter() - g0) * 1e3
+        del full
+
+    # e2e through the public API with pinned host inputs
+    e2e = None
+    if world == 1 and args.e2e_steps > 0:
+        from paper_2001_00532_b200._spindle import tensors as T
+
+        hA = DeviceTensor.from_arrays((A.M, A.N), "ds", {1: A.pos}, {1: A.crd}, A.vals32, dtype="f32", pin=True)
+        hB = DeviceTensor.dense(B, dtype="f32", pin=True)
+        hout = torch.empty(A.M * N, dtype=torch.float32).pin_memory()
+        h2d = hA.nbytes() + hB.nbytes()
+        d2h = hout.numel() * 4
+        interpret(prog, {"A": hA, "B": hB}, out=hout)  # warm
+        ts = []
+        for _ in range(args.e2e_steps):
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            interpret(prog, {"A": hA, "B": hB}, out=hout)  # H2D + launch + D2H + sync
+            ts.append(time.perf_counter() - t0)
+        e_t = statistics.median(ts)
+        e2e = {"value": round(flops / e_t / 1e9, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e_t * 1e3, 3)}
+        # parity spot check of the e2e result against the device result
+        ex.launch()
+        torch.cuda.synchronize(dev)
+        assert torch.equal(hout.view(-1), out.cpu().view(-1)), "e2e result differs from the device path"
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(A, B, 10_000_000)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_ms, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded R-MAT, BASELINE.md §3)",
+            "config": {"workload": WORKLOAD, "nnz": A.nnz, "M": A.M, "N": N,
+                       "schedule": prog.describe(), "parallelism": f"row-shards x{world}" if world > 1 else "1 GPU",
+                       "l2": "flushed (512 MB memset) before every timed step; inputs also > L2",
+                       "host_cpu": host_cpu_info()},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+            "step_ms_min": round(min(times), 4), "step_ms_max": round(max(times), 4),
+        }
+        if gather_ms is not None:
+            line["gather_ms"] = round(gather_ms, 3)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

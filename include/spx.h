@@ -1,0 +1,161 @@
+/*
+ * spx.h -- C-ABI of libspx.so, the B200 (sm_100a) backend for the scheduled
+ * sparse tensor algebra kernels of arXiv 2001.00532 (reference package
+ * `spindle`, mounted read-only at /root/reference/pkg/src/spindle).
+ *
+ * The reference ships no FFI and no lowering/execution modules: SPEC.md
+ * specifies them (`lower`, `interpret`, `emit_c`) and the
+ * only binary contract it fixes is the emitted-C entry point
+ *
+ *     void compute(double* out, const double** vals, const int32_t** pos,
+ *                  const int32_t** crd, const int32_t* dims);
+ *
+ * with the parameter order of `Manifest` (ir.py:237-263): one `vals` array
+ * per tensor in `Assignment.tensors` order (notation.py:202-209), one
+ * (pos, crd) pair per compressed level enumerated tensor-major then
+ * level-major (`Manifest.sparse_levels`, ir.py:257-263), and the input
+ * dimensions concatenated per tensor (`Manifest.dim_index`, ir.py:249-255).
+ *
+ * spx_launch() replaces that entry point.  It keeps the Manifest ordering
+ * for vals/pos/crd/dims and adds what a GPU launch needs: the selected
+ * kernel and its schedule constants (spx_plan), a caller-provided workspace
+ * and a CUDA stream.  All array arguments are DEVICE pointers; the pointer
+ * tables themselves (vals/pos/crd) and dims live in host memory.
+ *
+ * Ownership: every buffer is allocated and owned by the caller; the library
+ * never allocates or frees device memory.  Launches are asynchronous on the
+ * given stream.  The library is reentrant; the only global state is the
+ * per-thread error string and a launch counter.
+ *
+ * Error convention: every entry point returns an int status (0 = OK).
+ * The Python host maps the codes onto the reference hierarchy
+ * (errors.py:56-77):
+ *   SPX_E_ARG          -> SpindleError          (bad argument)
+ *   SPX_E_UNSUPPORTED  -> LoweringError         (errors.py:64-65)
+ *   SPX_E_CONTRACT     -> ContractViolation     (MaxExact, errors.py:76-77)
+ *   SPX_E_BOUNDS       -> OutOfBoundsError      (errors.py:72-73)
+ *   SPX_E_CUDA         -> ExecutionError        (errors.py:68-69)
+ *   SPX_E_WORKSPACE    -> ExecutionError        (workspace too small)
+ */
+#ifndef SPX_H_
+#define SPX_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPX_ABI_VERSION 1
+
+/* status codes */
+#define SPX_OK 0
+#define SPX_E_ARG 1
+#define SPX_E_UNSUPPORTED 2
+#define SPX_E_CONTRACT 3
+#define SPX_E_BOUNDS 4
+#define SPX_E_CUDA 5
+#define SPX_E_WORKSPACE 6
+
+/* value types (the reference is fp64 everywhere, tensors.py:253; the
+ * BASELINE configs 2-4 are fp32) */
+#define SPX_F64 0
+#define SPX_F32 1
+
+/*
+ * Kernel ids -- one per row of the schedule-shape selection table
+ * (DESIGN.md "Kernel table").  params[] carries the
+ * schedule constants of the matched shape:
+ *
+ *  id  kernel                    expression               params
+ *  1   SpMV row-split            y(i)=A(i,j)*x(j)  A:ds   [0]=ROWS_PER_TB
+ *  2   SpMV warp-per-row         "                        [0]=ROWS_PER_TB [1]=WARPS_PER_TB
+ *  3   SpMV nnz-split            "                        [0]=NNZ_PER_TB [1]=NNZ_PER_WARP [2]=NNZ_PER_THREAD
+ *  4   SpMM nnz-split            C(i,k)=A(i,j)*B(j,k)     [0]=NNZ_PER_TB [1]=NNZ_PER_WARP [2]=WARP_SIZE [3]=bound (0 = none)
+ *  5   SpMM warp-per-row         "                        [0]=ROWS_PER_TB [1]=WARPS_PER_TB [2]=WARP_SIZE [3]=bound
+ *  6   SDDMM nnz-split           A(i,j)=B(i,j)*C(i,k)*D(j,k)  [0]=NNZ_PER_TB [1]=NNZ_PER_WARP [2]=WARP_SIZE [3]=bound [7]=dense_out
+ *  7   TTV fiber-split           A(i,j)=B(i,j,k)*c(k) B:sss   [0]=FIBERS_PER_TB [1]=FIBERS_PER_WARP
+ *  8   MTTKRP nnz-split          A(i,j)=B(i,k,l)*C(k,j)*D(l,j) [0]=NNZ_PER_TB [1]=NNZ_PER_WARP [2]=WARP_SIZE [3]=bound
+ *  9   MTTKRP slice-split        "                        [0]=SLICES_PER_TB [1]=WARPS_PER_TB
+ *  10  SDDMM row-split           A(i,j)=B(i,j)*C(i,k)*D(j,k)  [0]=ROWS_PER_TB [1]=WARPS_PER_TB [2]=WARP_SIZE [3]=bound [7]=dense_out
+ *
+ * Operand roles: the kernels address operands by role, and slot[role] gives
+ * the role's index in the Manifest tensor order (vals[]/dims[] layout):
+ *   SpMV   role 0 = A (ds),  role 1 = x (d)            out = y[M]
+ *   SpMM   role 0 = A (ds),  role 1 = B (dd, K x N)    out = C[M x N]
+ *   SDDMM  role 0 = B (ds),  role 1 = C (dd, M x K), role 2 = D (dd, N x K)
+ *          out = nnz-aligned values [nnz]  (params[7]=1: dense M x N)
+ *   TTV    role 0 = B (sss), role 1 = c (d)            out = A[I x J]
+ *   MTTKRP role 0 = B (sss), role 1 = C (dd, K x R), role 2 = D (dd, L x R)
+ *          out = A[I x R]
+ * pos[]/crd[] hold the sparse operand's compressed levels in level order
+ * (exactly Manifest.sparse_levels for these expressions).
+ *
+ * level_sizes[] are the sparse operand's stored slot counts per level
+ * (Tensor.level_sizes(), tensors.py:135-145): CSR {M, nnz}; CSF {S, F, nnz}.
+ * They are passed so a launch never reads pos[] back to the host.
+ */
+#define SPX_K_SPMV_ROW 1
+#define SPX_K_SPMV_WARP 2
+#define SPX_K_SPMV_NNZ 3
+#define SPX_K_SPMM_NNZ 4
+#define SPX_K_SPMM_ROW 5
+#define SPX_K_SDDMM_NNZ 6
+#define SPX_K_TTV_FIBER 7
+#define SPX_K_MTTKRP_NNZ 8
+#define SPX_K_MTTKRP_SLICE 9
+#define SPX_K_SDDMM_ROW 10
+
+typedef struct spx_plan {
+  int32_t kernel_id;
+  int32_t dtype;
+  int32_t params[8];
+  int32_t slot[4];
+  int64_t level_sizes[4];
+} spx_plan;
+
+/* Replaces SPEC.md:447 `compute(out, vals, pos, crd, dims)`. */
+int spx_launch(const spx_plan* plan, void* out, const void* const* vals,
+               const int32_t* const* pos, const int32_t* const* crd,
+               const int32_t* dims, void* workspace, size_t ws_bytes,
+               void* stream);
+
+/* Workspace bytes spx_launch needs for this plan (0 if none). */
+size_t spx_workspace_size(const spx_plan* plan, const int32_t* dims);
+
+/* Thread-local message describing the last non-zero status. */
+const char* spx_last_error(void);
+
+/* Library ABI version (SPX_ABI_VERSION). */
+int spx_version(void);
+
+/* Total kernel launches issued by this library since load (all threads). */
+uint64_t spx_launch_count(void);
+
+/*
+ * Multi-GPU nnz-balanced segment partition -- the `divide` semantics of
+ * SPEC.md:248-256 on the fused position variable, snapped to segment
+ * boundaries:
+ *     chunk    = ceil(nnz / ndev)
+ *     target_g = min(g * chunk, nnz)
+ *     R_g      = first s in [0, nseg) with seg_start[s] >= target_g
+ *     R_0 = 0, R_ndev = nseg
+ * seg_start is a HOST array of nseg nondecreasing leaf offsets (CSR: pos[0..M)
+ * of the compressed level; CSF slices: pos2[pos1[s]]).  bounds_out receives
+ * ndev+1 entries.  Device g owns segments [R_g, R_{g+1}).
+ */
+int spx_partition(const int32_t* seg_start, int64_t nseg, int64_t nnz,
+                  int32_t ndev, int64_t* bounds_out);
+
+/* Same partition computed on the device from a DEVICE seg_start array
+ * (CSR pos of the compressed level, length >= nseg).  bounds_out is a DEVICE
+ * int64 array of ndev+1 entries. */
+int spx_partition_device(const int32_t* seg_start, int64_t nseg, int64_t nnz,
+                         int32_t ndev, int64_t* bounds_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPX_H_ */

@@ -1,0 +1,159 @@
+"""ctypes binding to libspx.so (C-ABI declared in include/spx.h).
+
+The library is required: there is no CPU fallback.  If libspx.so is missing
+the import of the execution path fails loudly with build instructions.
+Status codes are mapped onto the reference's error hierarchy
+(errors.py:56-77) exactly as include/spx.h documents.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+from . import _spindle
+
+LIB_PATH = Path(__file__).resolve().parent / "libspx.so"
+
+SPX_OK = 0
+SPX_E_ARG = 1
+SPX_E_UNSUPPORTED = 2
+SPX_E_CONTRACT = 3
+SPX_E_BOUNDS = 4
+SPX_E_CUDA = 5
+SPX_E_WORKSPACE = 6
+
+SPX_F64 = 0
+SPX_F32 = 1
+
+K_SPMV_ROW = 1
+K_SPMV_WARP = 2
+K_SPMV_NNZ = 3
+K_SPMM_NNZ = 4
+K_SPMM_ROW = 5
+K_SDDMM_NNZ = 6
+K_TTV_FIBER = 7
+K_MTTKRP_NNZ = 8
+K_MTTKRP_SLICE = 9
+K_SDDMM_ROW = 10
+
+KERNEL_NAMES = {
+    K_SPMV_ROW: "spmv_row",
+    K_SPMV_WARP: "spmv_warp",
+    K_SPMV_NNZ: "spmv_nnz",
+    K_SPMM_NNZ: "spmm_nnz",
+    K_SPMM_ROW: "spmm_row",
+    K_SDDMM_NNZ: "sddmm_nnz",
+    K_TTV_FIBER: "ttv_fiber",
+    K_MTTKRP_NNZ: "mttkrp_nnz",
+    K_MTTKRP_SLICE: "mttkrp_slice",
+    K_SDDMM_ROW: "sddmm_row",
+}
+
+# every symbol include/spx.h declares (checked by tests)
+EXPORTS = (
+    "spx_launch",
+    "spx_workspace_size",
+    "spx_last_error",
+    "spx_version",
+    "spx_launch_count",
+    "spx_partition",
+    "spx_partition_device",
+)
+
+
+class SpxPlan(ctypes.Structure):
+    _fields_ = [
+        ("kernel_id", ctypes.c_int32),
+        ("dtype", ctypes.c_int32),
+        ("params", ctypes.c_int32 * 8),
+        ("slot", ctypes.c_int32 * 4),
+        ("level_sizes", ctypes.c_int64 * 4),
+    ]
+
+
+_lib = None
+
+
+def load(path: str | os.PathLike | None = None):
+    """Load libspx.so (once).  Raises RuntimeError when it is not built."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        raise RuntimeError(
+            f"{p} is missing: the CUDA backend is not built "
+            "(run `python -m paper_2001_00532_b200.build` or __graft_entry__.build())"
+        )
+    lib = ctypes.CDLL(str(p))
+    vp = ctypes.c_void_p
+    i32p = ctypes.POINTER(ctypes.c_int32)
+    i64p = ctypes.POINTER(ctypes.c_int64)
+    lib.spx_launch.argtypes = [
+        ctypes.POINTER(SpxPlan),
+        vp,
+        ctypes.POINTER(vp),
+        ctypes.POINTER(vp),
+        ctypes.POINTER(vp),
+        i32p,
+        vp,
+        ctypes.c_size_t,
+        vp,
+    ]
+    lib.spx_launch.restype = ctypes.c_int
+    lib.spx_workspace_size.argtypes = [ctypes.POINTER(SpxPlan), i32p]
+    lib.spx_workspace_size.restype = ctypes.c_size_t
+    lib.spx_last_error.argtypes = []
+    lib.spx_last_error.restype = ctypes.c_char_p
+    lib.spx_version.argtypes = []
+    lib.spx_version.restype = ctypes.c_int
+    lib.spx_launch_count.argtypes = []
+    lib.spx_launch_count.restype = ctypes.c_uint64
+    lib.spx_partition.argtypes = [i32p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, i64p]
+    lib.spx_partition.restype = ctypes.c_int
+    lib.spx_partition_device.argtypes = [vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, vp, vp]
+    lib.spx_partition_device.restype = ctypes.c_int
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def last_error() -> str:
+    return load().spx_last_error().decode(errors="replace")
+
+
+def check(status: int, what: str = "spx") -> None:
+    """Raise the reference error class for a non-zero libspx status."""
+    if status == SPX_OK:
+        return
+    err = _spindle.errors
+    msg = f"{what}: {last_error()}"
+    if status == SPX_E_UNSUPPORTED:
+        raise err.LoweringError(msg)
+    if status == SPX_E_CONTRACT:
+        raise err.ContractViolation(msg)
+    if status == SPX_E_BOUNDS:
+        raise err.OutOfBoundsError(msg)
+    if status in (SPX_E_CUDA, SPX_E_WORKSPACE):
+        raise err.ExecutionError(msg)
+    raise err.SpindleError(msg)
+
+
+def launch_count() -> int:
+    return int(load().spx_launch_count())
+
+
+def ptr_array(ptrs) -> ctypes.Array:
+    arr = (ctypes.c_void_p * max(1, len(ptrs)))()
+    for k, p in enumerate(ptrs):
+        arr[k] = p
+    return arr
+
+
+def i32_array(vals) -> ctypes.Array:
+    arr = (ctypes.c_int32 * max(1, len(vals)))()
+    for k, v in enumerate(vals):
+        arr[k] = int(v)
+    return arr

@@ -1,0 +1,215 @@
+// Shared device helpers for the libspx kernels (sm_100a).
+//
+// Search semantics follow the reference IR exactly (ir.py:178-205):
+//   SearchSegment: largest s in [lo, hi) with arr[s] <= key, clamped to lo
+//   SearchCoord:   first s in [lo, hi) with arr[s] >= key, else hi
+// The oracle restates both in oracle/spx_oracle.c and tests compare them
+// bit for bit.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "spx_internal.h"
+
+namespace spx {
+
+constexpr unsigned kFull = 0xffffffffu;
+// Largest CTA any kernel is launched with; keeps the per-thread register
+// budget at 128 so the unrolled gathers stay in registers.
+constexpr int kMaxThreads = 512;
+constexpr int kMaxWarps = kMaxThreads / 32;
+
+// ---------------------------------------------------------------------------
+// cache-hinted loads/stores.  Streaming data (pos/crd/vals of the sparse
+// operand, outputs) is marked evict-first so the gathered dense operand keeps
+// its L2 residency (126 MB L2 vs 512 MB B at cfg2).
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ T ld_stream(const T* p) { return __ldcs(p); }
+template <typename T>
+__device__ __forceinline__ T ld_ro(const T* p) { return __ldg(p); }
+template <typename T>
+__device__ __forceinline__ void st_stream(T* p, T v) { __stcs(p, v); }
+
+// ---------------------------------------------------------------------------
+// Per-lane row fragments: a lane owns VPL values of a dense row.
+// CONTIG: lane owns columns [lane*VPL, lane*VPL+VPL) -> vector loads.
+// !CONTIG: lane owns columns {v*32 + lane} (the literal `split(k, dv,
+// thread, 32)` mapping of Appendix A.4) with a guard k < ncols.
+// ---------------------------------------------------------------------------
+template <typename T, int VPL, bool CONTIG>
+struct Frag {
+  T v[VPL];
+
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) v[i] = T(0);
+  }
+
+  __device__ __forceinline__ void load(const T* __restrict__ row, int lane, int ncols) {
+    if (CONTIG) {
+      const T* p = row + lane * VPL;
+      constexpr int BYTES = VPL * (int)sizeof(T);
+      if constexpr (BYTES % 16 == 0) {
+#pragma unroll
+        for (int c = 0; c < BYTES / 16; ++c) {
+          float4 q = __ldg(reinterpret_cast<const float4*>(p) + c);
+          *reinterpret_cast<float4*>(&v[c * (16 / sizeof(T))]) = q;
+        }
+      } else if constexpr (BYTES % 8 == 0) {
+#pragma unroll
+        for (int c = 0; c < BYTES / 8; ++c) {
+          float2 q = __ldg(reinterpret_cast<const float2*>(p) + c);
+          *reinterpret_cast<float2*>(&v[c * (8 / sizeof(T))]) = q;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < VPL; ++i) v[i] = __ldg(p + i);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) {
+        int k = i * 32 + lane;
+        v[i] = k < ncols ? __ldg(row + k) : T(0);
+      }
+    }
+  }
+
+  __device__ __forceinline__ void store(T* __restrict__ row, int lane, int ncols) const {
+    if (CONTIG) {
+      T* p = row + lane * VPL;
+      constexpr int BYTES = VPL * (int)sizeof(T);
+      if constexpr (BYTES % 16 == 0) {
+#pragma unroll
+        for (int c = 0; c < BYTES / 16; ++c)
+          __stcs(reinterpret_cast<float4*>(p) + c,
+                 *reinterpret_cast<const float4*>(&v[c * (16 / sizeof(T))]));
+      } else if constexpr (BYTES % 8 == 0) {
+#pragma unroll
+        for (int c = 0; c < BYTES / 8; ++c)
+          __stcs(reinterpret_cast<float2*>(p) + c,
+                 *reinterpret_cast<const float2*>(&v[c * (8 / sizeof(T))]));
+      } else {
+#pragma unroll
+        for (int i = 0; i < VPL; ++i) __stcs(p + i, v[i]);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) {
+        int k = i * 32 + lane;
+        if (k < ncols) __stcs(row + k, v[i]);
+      }
+    }
+  }
+
+  // read-modify-write add (used by the carry fix-ups; reads via L2 so a
+  // value written by another CTA/warp before the barrier/kernel boundary is
+  // observed)
+  __device__ __forceinline__ void add_into(T* __restrict__ row, int lane, int ncols) const {
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      int k = CONTIG ? lane * VPL + i : i * 32 + lane;
+      if (CONTIG || k < ncols) row[k] = __ldcg(row + k) + v[i];
+    }
+  }
+
+  __device__ __forceinline__ void atomic_add_into(T* __restrict__ row, int lane, int ncols) const {
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      int k = CONTIG ? lane * VPL + i : i * 32 + lane;
+      if (CONTIG || k < ncols) atomicAdd(row + k, v[i]);
+    }
+  }
+
+  // shared-memory staging uses the same per-lane layout as global memory
+  __device__ __forceinline__ void store_smem(T* row, int lane) const {
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) row[CONTIG ? lane * VPL + i : i * 32 + lane] = v[i];
+  }
+  __device__ __forceinline__ void add_smem(const T* row, int lane) {
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) v[i] += row[CONTIG ? lane * VPL + i : i * 32 + lane];
+  }
+
+  __device__ __forceinline__ void fma(T s, const Frag& b) {
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) v[i] = s * b.v[i] + v[i];
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Searches over nondecreasing int32 arrays (pos).
+// ---------------------------------------------------------------------------
+
+// ir.py:178-190 SearchSegment: largest s in [lo,hi) with arr[s] <= key,
+// clamped into [lo, hi).
+__device__ __forceinline__ int64_t search_segment(const int32_t* __restrict__ arr, int64_t lo,
+                                                  int64_t hi, int64_t key) {
+  if (hi <= lo) return lo;
+  int64_t a = lo, b = hi;  // find first index with arr[idx] > key in [lo,hi)
+  while (a < b) {
+    int64_t mid = (a + b) >> 1;
+    if ((int64_t)__ldg(arr + mid) <= key) a = mid + 1;
+    else b = mid;
+  }
+  int64_t s = a - 1;
+  return s < lo ? lo : s;
+}
+
+// first s in [lo,hi) with arr[s] >= key, else hi  (ir.py:193-205 semantics)
+__device__ __forceinline__ int64_t lower_bound(const int32_t* __restrict__ arr, int64_t lo,
+                                               int64_t hi, int64_t key) {
+  int64_t a = lo, b = hi;
+  while (a < b) {
+    int64_t mid = (a + b) >> 1;
+    if ((int64_t)__ldg(arr + mid) < key) a = mid + 1;
+    else b = mid;
+  }
+  return a;
+}
+
+// Warp-cooperative 32-ary SearchSegment: every lane returns the same result.
+// ceil(log32(hi-lo)) dependent steps instead of log2 (4 steps for 1M rows).
+__device__ __forceinline__ int64_t warp_search_segment(const int32_t* __restrict__ arr, int64_t lo,
+                                                       int64_t hi, int64_t key, int lane) {
+  if (hi <= lo) return lo;
+  int64_t a = lo, b = hi;  // answer in [a, b) if arr[a] <= key
+  while (b - a > 32) {
+    int64_t stride = (b - a + 31) >> 5;
+    int64_t idx = a + (int64_t)lane * stride;
+    bool ok = idx < b && (int64_t)__ldg(arr + idx) <= key;
+    unsigned m = __ballot_sync(kFull, ok);
+    if (m == 0) return lo == a ? lo : a;  // clamp: nothing <= key
+    int last = 31 - __clz(m);
+    int64_t na = a + (int64_t)last * stride;
+    int64_t nb = na + stride < b ? na + stride : b;
+    a = na;
+    b = nb;
+  }
+  int64_t idx = a + lane;
+  bool ok = idx < b && (int64_t)__ldg(arr + idx) <= key;
+  unsigned m = __ballot_sync(kFull, ok);
+  if (m == 0) return a;
+  return a + (31 - __clz(m));
+}
+
+// Per-warp cache of 32 consecutive row ends pos[base+1 .. base+32] held one
+// per lane, so row tracking ("step: while-advance over pos boundaries",
+// SPEC.md:364) costs a shuffle instead of a dependent global load.
+struct RowEndCache {
+  int64_t base;
+  int32_t mine;
+  __device__ __forceinline__ void fill(const int32_t* __restrict__ pos, int64_t r, int64_t nseg, int lane) {
+    base = r;
+    int64_t idx = r + 1 + lane;
+    mine = __ldg(pos + (idx < nseg ? idx : nseg));
+  }
+  // end of segment r (= pos[r+1]); r must be >= base
+  __device__ __forceinline__ int64_t end(const int32_t* __restrict__ pos, int64_t r, int64_t nseg, int lane) {
+    if (r - base >= 32) fill(pos, r, nseg, lane);
+    return (int64_t)__shfl_sync(kFull, mine, (int)(r - base));
+  }
+};
+
+}  // namespace spx

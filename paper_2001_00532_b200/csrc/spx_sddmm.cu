@@ -1,0 +1,234 @@
+// SDDMM kernels: A(i,j) = B(i,j) * C(i,k) * D(j,k) with B in CSR ("ds") and
+// C (M x K), D (N x K) dense row-major.  The result lives on B's pattern:
+// out[p] = B_vals[p] * <C[i,:], D[crd[p],:]>  (nnz-aligned, the sparse-output
+// extension of SURVEY.md §0.6 / §8(f) row 4); params[7]=1 scatters it into a
+// dense M x N output instead (the reference's dense-output semantics,
+// notation.py:156).
+//
+//  K6 SPX_K_SDDMM_NNZ: fuse(i,j,f) pos(f,fpos,B) split(fpos,block,..,NNZ_PER_TB)
+//     split(..,warp,nnz,NNZ_PER_WARP) split(k,dvu,thread,32)
+//     bound(dvu,dense_val,ceil(K/32),MaxExact), thread:Temporary.
+//     A warp walks NNZ_PER_WARP positions; lanes cover k; the 32 dot products
+//     of a batch are reduced with a 31-shuffle transpose-reduction so lane t
+//     ends with nonzero t's value and the store is coalesced.  Each position
+//     writes its own output: no races, no carries.
+//  K10 SPX_K_SDDMM_ROW: warp per row (row-split / unscheduled shapes).
+#include "spx_common.cuh"
+
+namespace spx {
+namespace {
+
+// part[t] on every lane -> lane t returns sum over lanes of part[t]
+template <typename T>
+__device__ __forceinline__ T transpose_reduce(T (&part)[32], int lane) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const bool upper = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < o; ++i) {
+      const T send = upper ? part[i] : part[i + o];
+      const T keep = upper ? part[i + o] : part[i];
+      part[i] = keep + __shfl_xor_sync(kFull, send, o);
+    }
+  }
+  return part[0];
+}
+
+template <typename T, int VPL, bool CONTIG>
+__device__ __forceinline__ T dot(const Frag<T, VPL, CONTIG>& a, const Frag<T, VPL, CONTIG>& b) {
+  T s = T(0);
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) s += a.v[i] * b.v[i];
+  return s;
+}
+
+template <typename T>
+__device__ __forceinline__ void emit(T* __restrict__ out, bool dense, int64_t N, int64_t p, int64_t r, int32_t c,
+                                     T val) {
+  if (dense) out[r * N + c] = val;
+  else __stcs(out + p, val);
+}
+
+// one batch of up to 32 positions starting at p, all of them in rows tracked
+// by (r, rend).  ROWFIXED: the caller guarantees a single row.
+template <typename T, int VPL, bool CONTIG, int U, bool ROWFIXED>
+__device__ __forceinline__ void sddmm_batch(const int32_t* __restrict__ pos, const int32_t* __restrict__ crd,
+                                            const T* __restrict__ vals, const T* __restrict__ Cm,
+                                            const T* __restrict__ Dm, T* __restrict__ out, int64_t M, int64_t N,
+                                            int64_t K, bool dense, int64_t p, int n, int64_t& r, int64_t& rend,
+                                            RowEndCache& ends, Frag<T, VPL, CONTIG>& crow, int lane) {
+  using F = Frag<T, VPL, CONTIG>;
+  int my_c = 0;
+  T my_v = T(0);
+  if (lane < n) {
+    my_c = __ldcs(crd + p + lane);
+    my_v = __ldcs(vals + p + lane);
+  }
+  // row of my position (for the dense scatter)
+  int64_t my_r = r;
+  T part[32];
+#pragma unroll
+  for (int t0 = 0; t0 < 32; t0 += U) {
+    F d[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int c = __shfl_sync(kFull, my_c, t0 + u);
+      if (t0 + u < n) d[u].load(Dm + (int64_t)c * K, lane, (int)K);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int t = t0 + u;
+      if (t < n) {
+        if (!ROWFIXED) {
+          const int64_t pp = p + t;
+          if (pp >= rend) {
+            while (pp >= rend) {
+              ++r;
+              rend = ends.end(pos, r, M, lane);
+            }
+            crow.load(Cm + r * K, lane, (int)K);
+          }
+          if (lane == t) my_r = r;
+        }
+        part[t] = dot(crow, d[u]);
+      } else {
+        part[t] = T(0);
+      }
+    }
+  }
+  const T s = transpose_reduce(part, lane);
+  if (lane < n) emit(out, dense, N, p + lane, my_r, my_c, my_v * s);
+}
+
+template <typename T, int VPL, bool CONTIG, int U>
+__global__ void __launch_bounds__(kMaxThreads) sddmm_nnz_kernel(const int32_t* __restrict__ pos,
+                                                         const int32_t* __restrict__ crd,
+                                                         const T* __restrict__ vals, const T* __restrict__ Cm,
+                                                         const T* __restrict__ Dm, T* __restrict__ out, int64_t M,
+                                                         int64_t N, int64_t K, int64_t nnz, int64_t TB, int64_t W,
+                                                         bool dense) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t p0 = (int64_t)blockIdx.x * TB;
+  const int64_t p1 = min(p0 + TB, nnz);
+  const int64_t q0 = min(p0 + (int64_t)warp * W, p1);
+  const int64_t q1 = min(q0 + W, p1);
+  if (q0 >= q1) return;
+  int64_t r = warp_search_segment(pos, 0, M, q0, lane);
+  RowEndCache ends;
+  ends.fill(pos, r, M, lane);
+  int64_t rend = ends.end(pos, r, M, lane);
+  Frag<T, VPL, CONTIG> crow;
+  crow.load(Cm + r * K, lane, (int)K);
+  for (int64_t p = q0; p < q1; p += 32) {
+    const int n = (int)min((int64_t)32, q1 - p);
+    sddmm_batch<T, VPL, CONTIG, U, false>(pos, crd, vals, Cm, Dm, out, M, N, K, dense, p, n, r, rend, ends, crow,
+                                          lane);
+  }
+}
+
+template <typename T, int VPL, bool CONTIG, int U>
+__global__ void __launch_bounds__(kMaxThreads) sddmm_row_kernel(const int32_t* __restrict__ pos,
+                                                         const int32_t* __restrict__ crd,
+                                                         const T* __restrict__ vals, const T* __restrict__ Cm,
+                                                         const T* __restrict__ Dm, T* __restrict__ out, int64_t M,
+                                                         int64_t N, int64_t K, int64_t R, bool dense) {
+  const int nw = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t lo = (int64_t)blockIdx.x * R;
+  const int64_t nwr = (R + nw - 1) / nw;
+  RowEndCache ends;  // unused on the fixed-row path
+  ends.base = 0;
+  ends.mine = 0;
+  for (int64_t wr = 0; wr < nwr; ++wr) {
+    const int64_t br = wr * nw + warp;
+    if (br >= R) break;
+    int64_t r = lo + br;
+    if (r >= M) break;
+    const int64_t a = __ldg(pos + r), e = __ldg(pos + r + 1);
+    if (a == e) continue;
+    Frag<T, VPL, CONTIG> crow;
+    crow.load(Cm + r * K, lane, (int)K);
+    int64_t rend = e;
+    for (int64_t p = a; p < e; p += 32) {
+      const int n = (int)min((int64_t)32, e - p);
+      sddmm_batch<T, VPL, CONTIG, U, true>(pos, crd, vals, Cm, Dm, out, M, N, K, dense, p, n, r, rend, ends, crow,
+                                           lane);
+    }
+  }
+}
+
+template <typename T, int VPL, bool CONTIG>
+int run_sddmm(int kid, const Args& a) {
+  constexpr int words = VPL * (int)sizeof(T) / 4;
+  constexpr int U = words >= 8 ? 4 : 8;
+  const int32_t* pos = a.pos[0];
+  const int32_t* crd = a.crd[0];
+  const T* vals = static_cast<const T*>(a.vals[0]);
+  const T* Cm = static_cast<const T*>(a.vals[1]);
+  const T* Dm = static_cast<const T*>(a.vals[2]);
+  T* out = static_cast<T*>(a.out);
+  const int64_t M = a.dims[0][0], N = a.dims[0][1], K = a.dims[1][1];
+  const int64_t nnz = a.level_sizes[1];
+  const bool dense = a.params[7] != 0;
+  if (dense) {
+    if (int e = check_cuda(cudaMemsetAsync(out, 0, (size_t)(M * N) * sizeof(T), a.stream), "memset")) return e;
+  }
+  if (M == 0 || nnz == 0) return SPX_OK;
+  if (kid == SPX_K_SDDMM_NNZ) {
+    const int64_t TB = a.params[0], W = a.params[1];
+    if (TB < 1 || W < 1 || TB % W != 0 || TB / W > kMaxWarps)
+      return fail(SPX_E_UNSUPPORTED, "SDDMM nnz-split needs NNZ_PER_TB a multiple of NNZ_PER_WARP, <= 16 warps");
+    sddmm_nnz_kernel<T, VPL, CONTIG, U><<<(unsigned)ceil_div(nnz, TB), (unsigned)(TB / W * 32), 0, a.stream>>>(
+        pos, crd, vals, Cm, Dm, out, M, N, K, nnz, TB, W, dense);
+    count_launch();
+    return check_cuda(cudaGetLastError(), "sddmm_nnz_kernel");
+  }
+  const int64_t R = a.params[0] > 0 ? a.params[0] : 8;
+  int64_t nw = a.params[1] > 0 ? a.params[1] : (R < 8 ? R : 8);
+  if (nw > kMaxWarps) nw = kMaxWarps;
+  sddmm_row_kernel<T, VPL, CONTIG, U><<<(unsigned)ceil_div(M, R), (unsigned)(nw * 32), 0, a.stream>>>(
+      pos, crd, vals, Cm, Dm, out, M, N, K, R, dense);
+  count_launch();
+  return check_cuda(cudaGetLastError(), "sddmm_row_kernel");
+}
+
+template <typename T>
+int dispatch_sddmm(int kid, const Args& a, int64_t K) {
+  const int vmax = sizeof(T) == 4 ? 8 : 4;
+  int v = (int)ceil_div(K < 1 ? 1 : K, 32), vpl = 1;
+  while (vpl < v) vpl <<= 1;
+  if (vpl > vmax)
+    return fail(SPX_E_UNSUPPORTED, "SDDMM supports K <= %d for this dtype, got %lld", 32 * vmax, (long long)K);
+  const bool contig = K == 32 * vpl;
+  switch (vpl * 2 + (contig ? 1 : 0)) {
+    case 2: return run_sddmm<T, 1, false>(kid, a);
+    case 3: return run_sddmm<T, 1, true>(kid, a);
+    case 4: return run_sddmm<T, 2, false>(kid, a);
+    case 5: return run_sddmm<T, 2, true>(kid, a);
+    case 8: return run_sddmm<T, 4, false>(kid, a);
+    case 9: return run_sddmm<T, 4, true>(kid, a);
+    default: break;
+  }
+  if constexpr (sizeof(T) == 4) {
+    if (vpl == 8) return contig ? run_sddmm<T, 8, true>(kid, a) : run_sddmm<T, 8, false>(kid, a);
+  }
+  return fail(SPX_E_UNSUPPORTED, "no SDDMM instantiation");
+}
+
+}  // namespace
+
+int launch_sddmm(int kid, const Args& a) {
+  const int64_t M = a.dims[0][0], N = a.dims[0][1], K = a.dims[1][1];
+  if (a.dims[1][0] != M || a.dims[2][0] != N || a.dims[2][1] != K)
+    return fail(SPX_E_ARG, "SDDMM: operand shapes disagree (B %lldx%lld, C %lldx%lld, D %lldx%lld)", (long long)M,
+                (long long)N, (long long)a.dims[1][0], (long long)K, (long long)a.dims[2][0],
+                (long long)a.dims[2][1]);
+  const int ws = a.params[2] ? a.params[2] : 32;
+  if (ws != 32) return fail(SPX_E_UNSUPPORTED, "split of k must be WARP_SIZE=32");
+  if (a.params[3] != 0 && (int64_t)a.params[3] != ceil_div(K, 32))
+    return fail(SPX_E_CONTRACT, "MaxExact bound violated: bound %d but ceil(%lld/32) = %lld", a.params[3],
+                (long long)K, (long long)ceil_div(K, 32));
+  return a.dtype == SPX_F32 ? dispatch_sddmm<float>(kid, a, K) : dispatch_sddmm<double>(kid, a, K);
+}
+
+}  // namespace spx

@@ -1,0 +1,373 @@
+// SpMM kernels: C(i,k) = A(i,j) * B(j,k), A in CSR ("ds"), B/C dense row-major.
+//
+//  K4 SPX_K_SPMM_NNZ  -- Appendix A.4:
+//      fuse(i,j,f) pos(f,fpos,A) split(fpos,block,fpos1,NNZ_PER_TB)
+//      split(fpos1,warp,nnz,NNZ_PER_WARP) split(k,dvu,thread,32)
+//      bound(dvu,dense_val,ceil(N/32),MaxExact)
+//    Each CTA owns NNZ_PER_TB consecutive nonzeros (the `block` variable),
+//    each warp NNZ_PER_WARP of them (`warp`), and the 32 lanes of a warp
+//    cover the dense row k (`thread`, `dense_val`).  The warp walks its
+//    positions sequentially (`nnz`) while tracking the row with a row-end
+//    cache (SPEC.md:364 Track recovery), gathering one 512 B row of B per
+//    nonzero with 16 B vector loads.
+//
+//    Output without a memset of C and without atomics: a row is *owned* by
+//    the chunk that holds its first position pos[r] (empty rows included,
+//    rows with pos[r]==nnz by the last chunk).  The owner stores its partial
+//    sum with a plain (streaming) store.  A chunk's only other row is its
+//    *head* row (the row holding the chunk's first position but starting
+//    before it); the head partial is parked in shared memory, summed across
+//    warps after the barrier and added onto the owner's value when the owner
+//    is in the same CTA, or written to a per-CTA carry slot that the fix-up
+//    kernel adds in CTA order (deterministic, SURVEY.md §7.3 "carry-out
+//    fixup").  This is the `Atomics` race strategy of the schedule realised
+//    without atomics.
+//
+//  K5 SPX_K_SPMM_ROW  -- warp-per-row (A.3/A.10/A.11 shapes and the GPU
+//    warp-per-row schedule): split(i,block,block_row,ROWS_PER_TB)
+//    split(block_row,warp_row,warp,WARPS) -> warp w of block b handles rows
+//    b*ROWS + warp_row*WARPS + w; lanes cover k.
+#include "spx_common.cuh"
+
+namespace spx {
+namespace {
+
+template <typename T, int VPL>
+constexpr int unroll_for() {
+  constexpr int words = VPL * (int)sizeof(T) / 4;  // 32-bit registers per fragment
+  constexpr int u = 32 / words;
+  return u > 8 ? 8 : (u < 2 ? 2 : u);
+}
+
+// first s in [lo,hi) with arr[s] >= key (warp-cooperative, 32-ary)
+__device__ __forceinline__ int64_t warp_lower_bound(const int32_t* __restrict__ arr, int64_t lo,
+                                                    int64_t hi, int64_t key, int lane) {
+  int64_t a = lo, b = hi;  // answer in [a, b]
+  while (b - a > 32) {
+    int64_t stride = (b - a + 31) >> 5;
+    int64_t idx = a + (int64_t)lane * stride;
+    bool lt = idx < b && (int64_t)__ldg(arr + idx) < key;
+    unsigned m = __ballot_sync(kFull, lt);
+    if (m == 0) return a;
+    int last = 31 - __clz(m);
+    int64_t na = a + (int64_t)last * stride + 1;
+    int64_t nb = a + (int64_t)(last + 1) * stride;
+    if (nb > b) nb = b;
+    a = na;
+    b = nb;
+  }
+  int64_t idx = a + lane;
+  bool lt = idx < b && (int64_t)__ldg(arr + idx) < key;
+  unsigned m = __ballot_sync(kFull, lt);
+  return a + __popc(m);
+}
+
+template <typename T, int VPL, bool CONTIG>
+__device__ __forceinline__ void store_zero_row(T* __restrict__ row, int lane, int ncols) {
+  Frag<T, VPL, CONTIG> z;
+  z.zero();
+  z.store(row, lane, ncols);
+}
+
+template <typename T, int VPL, bool CONTIG, int U>
+__global__ void __launch_bounds__(kMaxThreads) spmm_nnz_kernel(
+    const int32_t* __restrict__ pos, const int32_t* __restrict__ crd, const T* __restrict__ vals,
+    const T* __restrict__ B, T* __restrict__ C, int64_t M, int64_t N, int64_t nnz, int64_t TB,
+    int64_t W, int32_t* __restrict__ carry_row, T* __restrict__ carry_val) {
+  using F = Frag<T, VPL, CONTIG>;
+  constexpr int PW = 32 * VPL;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int nw = blockDim.x >> 5;
+  T* sval = reinterpret_cast<T*>(smem_raw);
+  int32_t* srow = reinterpret_cast<int32_t*>(sval + nw * PW);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t cta = blockIdx.x, ncta = gridDim.x;
+  const int64_t p0 = cta * TB;
+  const int64_t p1 = min(p0 + TB, nnz);
+  const int64_t q0 = min(p0 + (int64_t)warp * W, p1);
+  const int64_t q1 = min(q0 + W, p1);
+  const int64_t col0 = (int64_t)blockIdx.y * PW;
+  const int ncols = (int)min((int64_t)PW, N - col0);
+  const T* __restrict__ Bp = B + col0;
+  T* __restrict__ Cp = C + col0;
+
+  int32_t head = -1;
+  if (q0 < q1) {
+    int64_t r = warp_search_segment(pos, 0, M, q0, lane);  // row holding q0
+    const int64_t rstart = __ldg(pos + r);
+    bool is_head = rstart < q0;
+    if (!is_head && r > 0 && __ldg(pos + r - 1) == q0) {
+      // empty rows with pos == q0 sit before r and belong to this chunk
+      int64_t lb = warp_lower_bound(pos, 0, r, q0, lane);
+      for (int64_t rr = lb; rr < r; ++rr) store_zero_row<T, VPL, CONTIG>(Cp + rr * N, lane, ncols);
+    }
+    RowEndCache ends;
+    ends.fill(pos, r, M, lane);
+    int64_t rend = ends.end(pos, r, M, lane);
+    F acc;
+    acc.zero();
+    for (int64_t p = q0; p < q1; p += 32) {
+      const int n = (int)min((int64_t)32, q1 - p);
+      int my_c = 0;
+      T my_v = T(0);
+      if (lane < n) {
+        my_c = __ldcs(crd + p + lane);
+        my_v = __ldcs(vals + p + lane);
+      }
+      for (int t0 = 0; t0 < n; t0 += U) {
+        F b[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int c = __shfl_sync(kFull, my_c, (t0 + u) & 31);
+          if (t0 + u < n) b[u].load(Bp + (int64_t)c * N, lane, ncols);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (t0 + u < n) {
+            const T v = __shfl_sync(kFull, my_v, (t0 + u) & 31);
+            const int64_t pp = p + t0 + u;
+            while (pp >= rend) {
+              if (is_head) {
+                acc.store_smem(sval + warp * PW, lane);
+                head = (int32_t)r;
+                is_head = false;
+              } else {
+                acc.store(Cp + r * N, lane, ncols);
+              }
+              acc.zero();
+              ++r;
+              rend = ends.end(pos, r, M, lane);
+            }
+            acc.fma(v, b[u]);
+          }
+        }
+      }
+    }
+    if (is_head) {
+      acc.store_smem(sval + warp * PW, lane);
+      head = (int32_t)r;
+    } else {
+      acc.store(Cp + r * N, lane, ncols);
+    }
+    if (q1 == nnz) {
+      // trailing rows with pos[r] == nnz belong to the last chunk
+      for (int64_t rr = r + 1; rr < M; ++rr) store_zero_row<T, VPL, CONTIG>(Cp + rr * N, lane, ncols);
+    }
+  } else if (nnz == 0 && cta == 0) {
+    for (int64_t rr = warp; rr < M; rr += nw) store_zero_row<T, VPL, CONTIG>(Cp + rr * N, lane, ncols);
+  }
+  if (lane == 0) srow[warp] = head;
+  __syncthreads();
+
+  const int32_t hr = srow[warp];
+  const int64_t slot = (int64_t)blockIdx.y * ncta + cta;
+  if (hr >= 0 && (warp == 0 || srow[warp - 1] != hr)) {
+    F s;
+    s.zero();
+    s.add_smem(sval + warp * PW, lane);
+    for (int w2 = warp + 1; w2 < nw && srow[w2] == hr; ++w2) s.add_smem(sval + w2 * PW, lane);
+    if ((int64_t)__ldg(pos + hr) >= p0) {
+      s.add_into(Cp + (int64_t)hr * N, lane, ncols);  // owner stored before the barrier
+    } else {
+      s.store_smem(carry_val + slot * PW, lane);
+      if (lane == 0) carry_row[slot] = hr;
+    }
+  }
+  if (threadIdx.x == 0) {
+    const int32_t h0 = srow[0];
+    if (!(h0 >= 0 && (int64_t)__ldg(pos + h0) < p0)) carry_row[slot] = -1;
+  }
+}
+
+// Adds the per-CTA carries onto their rows.  The first CTA of a run of
+// equal carry rows sums the run in CTA order and updates C once.
+template <typename T, int VPL, bool CONTIG>
+__global__ void carry_fixup_kernel(const int32_t* __restrict__ carry_row, const T* __restrict__ carry_val,
+                                   T* __restrict__ C, int64_t N, int64_t nslots) {
+  using F = Frag<T, VPL, CONTIG>;
+  constexpr int PW = 32 * VPL;
+  const int lane = threadIdx.x & 31;
+  const int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (c >= nslots) return;
+  const int64_t base = (int64_t)blockIdx.y * nslots;
+  const int32_t row = carry_row[base + c];
+  if (row < 0) return;
+  if (c > 0 && carry_row[base + c - 1] == row) return;
+  const int64_t col0 = (int64_t)blockIdx.y * PW;
+  const int ncols = (int)min((int64_t)PW, N - col0);
+  F s;
+  s.zero();
+  for (int64_t c2 = c; c2 < nslots && carry_row[base + c2] == row; ++c2)
+    s.add_smem(carry_val + (base + c2) * PW, lane);
+  s.add_into(C + col0 + (int64_t)row * N, lane, ncols);
+}
+
+template <typename T, int VPL, bool CONTIG, int U>
+__global__ void __launch_bounds__(kMaxThreads) spmm_row_kernel(
+    const int32_t* __restrict__ pos, const int32_t* __restrict__ crd, const T* __restrict__ vals,
+    const T* __restrict__ B, T* __restrict__ C, int64_t M, int64_t N, int64_t R) {
+  using F = Frag<T, VPL, CONTIG>;
+  constexpr int PW = 32 * VPL;
+  const int nw = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t col0 = (int64_t)blockIdx.y * PW;
+  const int ncols = (int)min((int64_t)PW, N - col0);
+  const T* __restrict__ Bp = B + col0;
+  T* __restrict__ Cp = C + col0;
+  const int64_t rows_lo = (int64_t)blockIdx.x * R;
+  const int64_t nwr = (R + nw - 1) / nw;
+  for (int64_t wr = 0; wr < nwr; ++wr) {
+    const int64_t br = wr * nw + warp;  // block_row = warp_row*WARPS + warp
+    if (br >= R) break;
+    const int64_t row = rows_lo + br;
+    if (row >= M) break;
+    const int64_t a = __ldg(pos + row), e = __ldg(pos + row + 1);
+    F acc;
+    acc.zero();
+    for (int64_t p = a; p < e; p += 32) {
+      const int n = (int)min((int64_t)32, e - p);
+      int my_c = 0;
+      T my_v = T(0);
+      if (lane < n) {
+        my_c = __ldcs(crd + p + lane);
+        my_v = __ldcs(vals + p + lane);
+      }
+      for (int t0 = 0; t0 < n; t0 += U) {
+        F b[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int c = __shfl_sync(kFull, my_c, (t0 + u) & 31);
+          if (t0 + u < n) b[u].load(Bp + (int64_t)c * N, lane, ncols);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const T v = __shfl_sync(kFull, my_v, (t0 + u) & 31);
+          if (t0 + u < n) acc.fma(v, b[u]);
+        }
+      }
+    }
+    acc.store(Cp + row * N, lane, ncols);
+  }
+}
+
+struct SpmmGeom {
+  int vpl;
+  int pw;
+  int npanels;
+  bool contig;
+};
+
+SpmmGeom spmm_geom(int dtype, int64_t N) {
+  const int vmax = dtype == SPX_F32 ? 8 : 4;
+  int v = (int)ceil_div(N < 1 ? 1 : N, 32);
+  int vpl = 1;
+  while (vpl < v && vpl < vmax) vpl <<= 1;
+  SpmmGeom g;
+  g.vpl = vpl;
+  g.pw = 32 * vpl;
+  g.npanels = (int)ceil_div(N < 1 ? 1 : N, g.pw);
+  g.contig = (N % g.pw) == 0;
+  return g;
+}
+
+int check_bound(const Args& a, int64_t N) {
+  const int ws = a.params[2] ? a.params[2] : 32;
+  if (ws != 32)
+    return fail(SPX_E_UNSUPPORTED, "split of the dense dimension must be WARP_SIZE=32, got %d", ws);
+  const int b = a.params[3];
+  if (b != 0 && (int64_t)b != ceil_div(N, 32))
+    return fail(SPX_E_CONTRACT,
+                "MaxExact bound violated: dense_val bound %d but the runtime extent ceil(%lld/32) is %lld",
+                b, (long long)N, (long long)ceil_div(N, 32));
+  return SPX_OK;
+}
+
+template <typename T, int VPL, bool CONTIG>
+int run_spmm(int kid, const Args& a, const SpmmGeom& g) {
+  constexpr int U = unroll_for<T, VPL>();
+  const int32_t* pos = a.pos[0];
+  const int32_t* crd = a.crd[0];
+  const T* vals = static_cast<const T*>(a.vals[0]);
+  const T* B = static_cast<const T*>(a.vals[1]);
+  T* C = static_cast<T*>(a.out);
+  const int64_t M = a.dims[0][0], N = a.dims[1][1];
+  const int64_t nnz = a.level_sizes[1];
+  if (M == 0 || N == 0) return SPX_OK;
+  if (kid == SPX_K_SPMM_NNZ) {
+    const int64_t TB = a.params[0], W = a.params[1];
+    if (TB < 1 || W < 1 || TB % W != 0 || TB / W > kMaxWarps)
+      return fail(SPX_E_UNSUPPORTED,
+                  "SpMM nnz-split needs NNZ_PER_TB a multiple of NNZ_PER_WARP with <= 16 warps (got %lld, %lld)",
+                  (long long)TB, (long long)W);
+    const int nw = (int)(TB / W);
+    const int64_t ncta = nnz == 0 ? 1 : ceil_div(nnz, TB);
+    if (ncta > INT32_MAX) return fail(SPX_E_ARG, "grid too large");
+    const size_t need = (size_t)ncta * g.npanels * (sizeof(int32_t) + (size_t)g.pw * sizeof(T)) + 256;
+    if (a.ws_bytes < need || !a.ws) return fail(SPX_E_WORKSPACE, "workspace %zu < %zu bytes", a.ws_bytes, need);
+    T* carry_val = static_cast<T*>(a.ws);
+    int32_t* carry_row = reinterpret_cast<int32_t*>(
+        reinterpret_cast<char*>(a.ws) + (((size_t)ncta * g.npanels * g.pw * sizeof(T) + 255) & ~(size_t)255));
+    const size_t smem = (size_t)nw * (g.pw * sizeof(T) + sizeof(int32_t));
+    dim3 grid((unsigned)ncta, (unsigned)g.npanels);
+    spmm_nnz_kernel<T, VPL, CONTIG, U><<<grid, nw * 32, smem, a.stream>>>(pos, crd, vals, B, C, M, N, nnz, TB,
+                                                                          W, carry_row, carry_val);
+    count_launch();
+    if (int e = check_cuda(cudaGetLastError(), "spmm_nnz_kernel")) return e;
+    const int fw = 8;
+    dim3 fgrid((unsigned)ceil_div(ncta, fw), (unsigned)g.npanels);
+    carry_fixup_kernel<T, VPL, CONTIG><<<fgrid, fw * 32, 0, a.stream>>>(carry_row, carry_val, C, N, ncta);
+    count_launch();
+    return check_cuda(cudaGetLastError(), "carry_fixup_kernel");
+  }
+  // warp-per-row
+  const int64_t R = a.params[0] > 0 ? a.params[0] : 8;
+  int64_t nw = a.params[1] > 0 ? a.params[1] : (R < 8 ? R : 8);
+  if (nw > kMaxWarps) nw = kMaxWarps;
+  dim3 grid((unsigned)ceil_div(M, R), (unsigned)g.npanels);
+  spmm_row_kernel<T, VPL, CONTIG, U><<<grid, (unsigned)(nw * 32), 0, a.stream>>>(pos, crd, vals, B, C, M, N, R);
+  count_launch();
+  return check_cuda(cudaGetLastError(), "spmm_row_kernel");
+}
+
+template <typename T>
+int dispatch_spmm(int kid, const Args& a, const SpmmGeom& g) {
+  switch (g.vpl * 2 + (g.contig ? 1 : 0)) {
+    case 2: return run_spmm<T, 1, false>(kid, a, g);
+    case 3: return run_spmm<T, 1, true>(kid, a, g);
+    case 4: return run_spmm<T, 2, false>(kid, a, g);
+    case 5: return run_spmm<T, 2, true>(kid, a, g);
+    case 8: return run_spmm<T, 4, false>(kid, a, g);
+    case 9: return run_spmm<T, 4, true>(kid, a, g);
+    default: break;
+  }
+  if constexpr (sizeof(T) == 4) {
+    if (g.vpl == 8) return g.contig ? run_spmm<T, 8, true>(kid, a, g) : run_spmm<T, 8, false>(kid, a, g);
+  }
+  return fail(SPX_E_UNSUPPORTED, "no SpMM instantiation for %d values per lane", g.vpl);
+}
+
+}  // namespace
+
+size_t ws_spmm(int kid, const Args& a) {
+  if (kid != SPX_K_SPMM_NNZ) return 0;
+  const int64_t N = a.dims[1][1];
+  const SpmmGeom g = spmm_geom(a.dtype, N);
+  const int64_t nnz = a.level_sizes[1];
+  const int64_t TB = a.params[0] > 0 ? a.params[0] : 1;
+  const int64_t ncta = nnz == 0 ? 1 : ceil_div(nnz, TB);
+  const size_t es = a.dtype == SPX_F32 ? 4 : 8;
+  return (size_t)ncta * g.npanels * (sizeof(int32_t) + (size_t)g.pw * es) + 256;
+}
+
+int launch_spmm(int kid, const Args& a) {
+  const int64_t M = a.dims[0][0], K = a.dims[0][1];
+  if (a.dims[1][0] != K) return fail(SPX_E_ARG, "SpMM: A is %lld x %lld but B has %lld rows", (long long)M,
+                                     (long long)K, (long long)a.dims[1][0]);
+  const int64_t N = a.dims[1][1];
+  if (int e = check_bound(a, N)) return e;
+  const SpmmGeom g = spmm_geom(a.dtype, N);
+  return a.dtype == SPX_F32 ? dispatch_spmm<float>(kid, a, g) : dispatch_spmm<double>(kid, a, g);
+}
+
+}  // namespace spx

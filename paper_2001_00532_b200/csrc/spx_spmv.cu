@@ -1,0 +1,324 @@
+// SpMV kernels: y(i) = A(i,j) * x(j), A in CSR ("ds"), x and y dense.
+//
+//  K1 SPX_K_SPMV_ROW  -- thread per row: A.7 `split(i,block,thread,ROWS_PER_TB)`
+//     (PAPER.md:2004-2016), also the A.1 CPU shape `split(i,i0,i1,CHUNK)`
+//      and the unscheduled statement.
+//  K2 SPX_K_SPMV_WARP -- warp per row, A.8:
+//     split(i,block,block_row,ROWS_PER_TB) split(block_row,warp_row,warp,W)
+//     pos(j,jpos,A) split(jpos,thread_nz,thread,32), thread:Temporary -> the
+//     lanes stride the row's positions and fold with a shuffle tree.
+//  K3 SPX_K_SPMV_NNZ  -- position-split, A.2/A.9 (PAPER.md:1902-1925,
+//     2039-2057): fuse(i,j,f) pos(f,fpos,A) split(fpos,block,..,NNZ_PER_TB)
+//     split(..,warp,..,NNZ_PER_WARP) split(..,thread,thread_nz,NNZ_PER_THREAD).
+//     Thread t of a CTA owns NNZ_PER_THREAD consecutive positions
+//     (`thread_nz` innermost, exactly the schedule), loads them with 16 B
+//     vector loads, tracks the row through a shared-memory copy of the CTA's
+//     slice of pos (Track recovery), stores rows it owns and
+//     parks its head partial (the `Atomics` output race) in shared memory;
+//     runs of equal head rows are folded after the barrier and CTA-spanning
+//     rows go through the deterministic carry fix-up (see spx_spmm.cu).
+#include "spx_common.cuh"
+
+namespace spx {
+namespace {
+
+constexpr int kPosCache = 4096;  // ints of pos staged per CTA
+
+template <typename T>
+__global__ void __launch_bounds__(kMaxThreads) spmv_row_kernel(const int32_t* __restrict__ pos,
+                                                        const int32_t* __restrict__ crd,
+                                                        const T* __restrict__ vals, const T* __restrict__ x,
+                                                        T* __restrict__ y, int64_t M, int64_t R) {
+  const int64_t lo = (int64_t)blockIdx.x * R;
+  for (int64_t t = threadIdx.x; t < R; t += blockDim.x) {
+    const int64_t i = lo + t;
+    if (i >= M) return;
+    const int64_t a = __ldg(pos + i), e = __ldg(pos + i + 1);
+    T acc = T(0);
+    for (int64_t p = a; p < e; ++p) acc += __ldcs(vals + p) * __ldg(x + __ldcs(crd + p));
+    __stcs(y + i, acc);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kMaxThreads) spmv_warp_kernel(const int32_t* __restrict__ pos,
+                                                         const int32_t* __restrict__ crd,
+                                                         const T* __restrict__ vals, const T* __restrict__ x,
+                                                         T* __restrict__ y, int64_t M, int64_t R) {
+  const int nw = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t lo = (int64_t)blockIdx.x * R;
+  const int64_t nwr = (R + nw - 1) / nw;
+  for (int64_t wr = 0; wr < nwr; ++wr) {
+    const int64_t br = wr * nw + warp;
+    if (br >= R) break;
+    const int64_t i = lo + br;
+    if (i >= M) break;
+    const int64_t a = __ldg(pos + i), e = __ldg(pos + i + 1);
+    T acc = T(0);
+    for (int64_t p = a + lane; p < e; p += 32) acc += __ldcs(vals + p) * __ldg(x + __ldcs(crd + p));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+    if (lane == 0) __stcs(y + i, acc);
+  }
+}
+
+// Loads NNZ_PER_THREAD consecutive (crd, vals) with vector loads when the
+// count is a compile-time multiple of 4 and the chunk is full.
+template <typename T, int TPT>
+struct ThreadChunk {
+  int32_t c[TPT];
+  T v[TPT];
+  __device__ __forceinline__ void load(const int32_t* __restrict__ crd, const T* __restrict__ vals, int64_t a,
+                                       int n) {
+    if (TPT % 4 == 0 && n == TPT) {
+#pragma unroll
+      for (int k = 0; k < TPT / 4; ++k) {
+        int4 q = __ldcs(reinterpret_cast<const int4*>(crd + a) + k);
+        c[4 * k] = q.x;
+        c[4 * k + 1] = q.y;
+        c[4 * k + 2] = q.z;
+        c[4 * k + 3] = q.w;
+      }
+      constexpr int per16 = 16 / (int)sizeof(T);
+#pragma unroll
+      for (int k = 0; k < TPT / per16; ++k) {
+        float4 q = __ldcs(reinterpret_cast<const float4*>(vals + a) + k);
+        *reinterpret_cast<float4*>(&v[k * per16]) = q;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < TPT; ++k) {
+        c[k] = k < n ? __ldcs(crd + a + k) : 0;
+        v[k] = k < n ? __ldcs(vals + a + k) : T(0);
+      }
+    }
+  }
+};
+
+// TPT > 0: compile-time NNZ_PER_THREAD; TPT == 0: runtime `tpt`.
+template <typename T, int TPT>
+__global__ void __launch_bounds__(kMaxThreads) spmv_nnz_kernel(const int32_t* __restrict__ pos,
+                                                        const int32_t* __restrict__ crd,
+                                                        const T* __restrict__ vals, const T* __restrict__ x,
+                                                        T* __restrict__ y, int64_t M, int64_t nnz, int64_t TB,
+                                                        int tpt_rt, int32_t* __restrict__ carry_row,
+                                                        T* __restrict__ carry_val) {
+  __shared__ int32_t s_pos[kPosCache];
+  __shared__ int64_t s_rows[2];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* s_hval = reinterpret_cast<T*>(smem_raw);
+  int32_t* s_hrow = reinterpret_cast<int32_t*>(s_hval + blockDim.x);
+
+  const int tpt = TPT > 0 ? TPT : tpt_rt;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int64_t cta = blockIdx.x;
+  const int64_t p0 = cta * TB;
+  const int64_t p1 = min(p0 + TB, nnz);
+  const int64_t a = min(p0 + (int64_t)tid * tpt, p1);
+  const int64_t e = min(a + tpt, p1);
+
+  if (p0 < p1) {
+    if (tid < 32) {
+      const int64_t rlo = warp_search_segment(pos, 0, M, p0, lane);
+      const int64_t rhi = warp_search_segment(pos, rlo, M, p1 - 1, lane);
+      if (lane == 0) {
+        s_rows[0] = rlo;
+        s_rows[1] = rhi;
+      }
+    }
+    __syncthreads();
+    const int64_t rlo = s_rows[0], rhi = s_rows[1];
+    const int64_t nstage = rhi - rlo + 2;  // pos[rlo .. rhi+1]
+    const bool staged = nstage <= kPosCache;
+    if (staged)
+      for (int64_t k = tid; k < nstage; k += blockDim.x) s_pos[k] = __ldg(pos + rlo + k);
+    __syncthreads();
+    auto P = [&](int64_t r) -> int64_t {  // pos[r] for r in [rlo, rhi+1]
+      return staged ? (int64_t)s_pos[r - rlo] : (int64_t)__ldg(pos + r);
+    };
+
+    int32_t head = -1;
+    T hval = T(0);
+    if (a < e) {
+      // SearchSegment over the CTA's rows (ir.py:178-190)
+      int64_t lo = rlo, hi = rhi + 1;
+      while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        if (P(mid) <= a) lo = mid + 1;
+        else hi = mid;
+      }
+      int64_t r = lo - 1;
+      bool is_head = P(r) < a;
+      if (!is_head && r > 0) {
+        // empty rows with pos == a before r are owned by this thread
+        int64_t rr = r - 1;
+        while (rr >= rlo && P(rr) == a) __stcs(y + rr--, T(0));
+        if (rr < rlo && rr >= 0 && __ldg(pos + rr) == a) {
+          int64_t lb = lower_bound(pos, 0, rlo, a);
+          for (int64_t q = lb; q < rlo; ++q) __stcs(y + q, T(0));
+        }
+      }
+      int64_t rend = P(r + 1);
+      T acc = T(0);
+      const int n = (int)(e - a);
+      if constexpr (TPT > 0) {
+        ThreadChunk<T, TPT> ch;
+        ch.load(crd, vals, a, n);
+        T xv[TPT];
+#pragma unroll
+        for (int k = 0; k < TPT; ++k) xv[k] = k < n ? __ldg(x + ch.c[k]) : T(0);
+#pragma unroll
+        for (int k = 0; k < TPT; ++k) {
+          if (k < n) {
+            const int64_t p = a + k;
+            while (p >= rend) {
+              if (is_head) {
+                head = (int32_t)r;
+                hval = acc;
+                is_head = false;
+              } else {
+                __stcs(y + r, acc);
+              }
+              acc = T(0);
+              ++r;
+              rend = P(r + 1);
+            }
+            acc += ch.v[k] * xv[k];
+          }
+        }
+      } else {
+        for (int64_t p = a; p < e; ++p) {
+          const T prod = __ldcs(vals + p) * __ldg(x + __ldcs(crd + p));
+          while (p >= rend) {
+            if (is_head) {
+              head = (int32_t)r;
+              hval = acc;
+              is_head = false;
+            } else {
+              __stcs(y + r, acc);
+            }
+            acc = T(0);
+            ++r;
+            rend = P(r + 1);
+          }
+          acc += prod;
+        }
+      }
+      if (is_head) {
+        head = (int32_t)r;
+        hval = acc;
+      } else {
+        __stcs(y + r, acc);
+      }
+      if (e == nnz)
+        for (int64_t q = r + 1; q < M; ++q) __stcs(y + q, T(0));
+    }
+    s_hrow[tid] = head;
+    s_hval[tid] = hval;
+    __syncthreads();
+    if (head >= 0 && (tid == 0 || s_hrow[tid - 1] != head)) {
+      T s = hval;
+      for (int t2 = tid + 1; t2 < (int)blockDim.x && s_hrow[t2] == head; ++t2) s += s_hval[t2];
+      if (P(head) >= p0) {
+        y[head] = __ldcg(y + head) + s;
+      } else {
+        carry_val[cta] = s;
+        carry_row[cta] = head;
+      }
+    }
+    if (tid == 0 && !(head >= 0 && P(head) < p0)) carry_row[cta] = -1;
+  } else {
+    if (nnz == 0 && cta == 0)
+      for (int64_t q = tid; q < M; q += blockDim.x) __stcs(y + q, T(0));
+    if (tid == 0) carry_row[cta] = -1;
+  }
+}
+
+template <typename T>
+__global__ void spmv_fixup_kernel(const int32_t* __restrict__ carry_row, const T* __restrict__ carry_val,
+                                  T* __restrict__ y, int64_t n) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  const int32_t row = carry_row[c];
+  if (row < 0 || (c > 0 && carry_row[c - 1] == row)) return;
+  T s = T(0);
+  for (int64_t c2 = c; c2 < n && carry_row[c2] == row; ++c2) s += carry_val[c2];
+  y[row] = __ldcg(y + row) + s;
+}
+
+template <typename T>
+int run_spmv(int kid, const Args& a) {
+  const int32_t* pos = a.pos[0];
+  const int32_t* crd = a.crd[0];
+  const T* vals = static_cast<const T*>(a.vals[0]);
+  const T* x = static_cast<const T*>(a.vals[1]);
+  T* y = static_cast<T*>(a.out);
+  const int64_t M = a.dims[0][0];
+  const int64_t nnz = a.level_sizes[1];
+  if (M == 0) return SPX_OK;
+  if (kid == SPX_K_SPMV_ROW) {
+    const int64_t R = a.params[0] > 0 ? a.params[0] : 256;
+    const int threads = (int)(R < 256 ? (R < 32 ? 32 : R) : 256);
+    spmv_row_kernel<T><<<(unsigned)ceil_div(M, R), threads, 0, a.stream>>>(pos, crd, vals, x, y, M, R);
+    count_launch();
+    return check_cuda(cudaGetLastError(), "spmv_row_kernel");
+  }
+  if (kid == SPX_K_SPMV_WARP) {
+    const int64_t R = a.params[0] > 0 ? a.params[0] : 8;
+    int64_t nw = a.params[1] > 0 ? a.params[1] : (R < 8 ? R : 8);
+    if (nw > kMaxWarps) nw = kMaxWarps;
+    spmv_warp_kernel<T><<<(unsigned)ceil_div(M, R), (unsigned)(nw * 32), 0, a.stream>>>(pos, crd, vals, x, y, M, R);
+    count_launch();
+    return check_cuda(cudaGetLastError(), "spmv_warp_kernel");
+  }
+  // nnz-split
+  const int64_t TB = a.params[0], W = a.params[1], TPT = a.params[2];
+  if (TB < 1 || W < 1 || TPT < 1 || W != 32 * TPT || TB % W != 0 || TB / TPT > kMaxThreads)
+    return fail(SPX_E_UNSUPPORTED,
+                "SpMV nnz-split needs NNZ_PER_WARP == 32*NNZ_PER_THREAD and NNZ_PER_TB a multiple of "
+                "NNZ_PER_WARP with <= 512 threads (got %lld, %lld, %lld)",
+                (long long)TB, (long long)W, (long long)TPT);
+  const int threads = (int)(TB / TPT);
+  const int64_t ncta = nnz == 0 ? 1 : ceil_div(nnz, TB);
+  const size_t need = (size_t)ncta * (sizeof(T) + sizeof(int32_t)) + 256;
+  if (!a.ws || a.ws_bytes < need) return fail(SPX_E_WORKSPACE, "workspace %zu < %zu bytes", a.ws_bytes, need);
+  T* carry_val = static_cast<T*>(a.ws);
+  int32_t* carry_row =
+      reinterpret_cast<int32_t*>(reinterpret_cast<char*>(a.ws) + ((ncta * sizeof(T) + 255) & ~(size_t)255));
+  const size_t smem = (size_t)threads * (sizeof(T) + sizeof(int32_t));
+  const unsigned g = (unsigned)ncta;
+  switch (TPT) {
+    case 4: spmv_nnz_kernel<T, 4><<<g, threads, smem, a.stream>>>(pos, crd, vals, x, y, M, nnz, TB, 4, carry_row, carry_val); break;
+    case 8: spmv_nnz_kernel<T, 8><<<g, threads, smem, a.stream>>>(pos, crd, vals, x, y, M, nnz, TB, 8, carry_row, carry_val); break;
+    case 16: spmv_nnz_kernel<T, 16><<<g, threads, smem, a.stream>>>(pos, crd, vals, x, y, M, nnz, TB, 16, carry_row, carry_val); break;
+    default:
+      spmv_nnz_kernel<T, 0><<<g, threads, smem, a.stream>>>(pos, crd, vals, x, y, M, nnz, TB, (int)TPT, carry_row,
+                                                            carry_val);
+  }
+  count_launch();
+  if (int e = check_cuda(cudaGetLastError(), "spmv_nnz_kernel")) return e;
+  spmv_fixup_kernel<T><<<(unsigned)ceil_div(ncta, 256), 256, 0, a.stream>>>(carry_row, carry_val, y, ncta);
+  count_launch();
+  return check_cuda(cudaGetLastError(), "spmv_fixup_kernel");
+}
+
+}  // namespace
+
+size_t ws_spmv(int kid, const Args& a) {
+  if (kid != SPX_K_SPMV_NNZ) return 0;
+  const int64_t nnz = a.level_sizes[1];
+  const int64_t TB = a.params[0] > 0 ? a.params[0] : 1;
+  const int64_t ncta = nnz == 0 ? 1 : ceil_div(nnz, TB);
+  const size_t es = a.dtype == SPX_F32 ? 4 : 8;
+  return (size_t)ncta * (es + sizeof(int32_t)) + 256;
+}
+
+int launch_spmv(int kid, const Args& a) {
+  if (a.dims[1][0] != a.dims[0][1])
+    return fail(SPX_E_ARG, "SpMV: A has %lld columns but x has %lld entries", (long long)a.dims[0][1],
+                (long long)a.dims[1][0]);
+  return a.dtype == SPX_F32 ? run_spmv<float>(kid, a) : run_spmv<double>(kid, a);
+}
+
+}  // namespace spx

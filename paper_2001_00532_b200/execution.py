@@ -1,0 +1,339 @@
+"""`interpret`: run a lowered Program on the GPU.
+
+SPEC's interpreter is the normative semantics of a scheduled kernel; here the
+same contract -- `interpret(program, inputs, out_dims) -> (DenseTensor,
+ExecStats)` -- is met by launching the selected sm_100a kernel through the
+C-ABI (spx_launch, include/spx.h).  Inputs may be reference `Tensor` /
+`DenseTensor` / ndarray values on the host (copied to HBM inside the call)
+or device-resident `DeviceTensor`s.
+
+`ExecStats` is reproduced exactly on the host from the
+schedule's partition: per-parallel-instance work (leaf positions handled by
+each block / warp / thread), loop extents and split-tail guard failures.
+
+There is no CPU fallback: a missing libspx.so or a missing CUDA device raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from functools import cached_property
+
+import numpy as np
+import torch
+
+from . import _lib, _spindle
+from .formats import DeviceTensor, as_device_operand, dtype_name, torch_dtype
+from .lowering import Program
+
+# SDDMM results larger than this many dense elements are returned on B's
+# pattern (the nnz-aligned sparse-output extension) unless asked otherwise
+DENSE_SDDMM_LIMIT = 1 << 27
+
+
+def _cur_stream(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+class Executor:
+    """A Program bound to device operands and an output buffer.
+
+    Construction resolves the Manifest-ordered argument tables once
+    (ir.py:237-263), sizes and allocates the workspace, and builds the
+    spx_plan; `launch` is then a single C call, cheap enough to sit in a
+    timed loop or a CUDA-graph capture.
+    """
+
+    def __init__(self, program: Program, operands: dict, out: torch.Tensor, *, dtype: str,
+                 dense_out: bool | None = None):
+        self.program = program
+        self.dtype = dtype
+        self.operands = operands
+        self.out = out
+        lib = _lib.load()
+        order = program.tensor_order
+        sp = operands[program.ec.tensors[0]]
+        self.sparse = sp
+        self.dims_map = {t: operands[t].dims for t in order}
+        dims = [d for t in order for d in operands[t].dims]
+        self._dims = _lib.i32_array(dims)
+        self._vals = _lib.ptr_array([operands[t].vals.data_ptr() for t in order])
+        lvls = [lv for lv, ch in enumerate(sp.levels) if ch == "s"]
+        self._pos = _lib.ptr_array([sp.pos[lv].data_ptr() for lv in lvls])
+        self._crd = _lib.ptr_array([sp.crd[lv].data_ptr() for lv in lvls])
+        self.level_sizes = sp.level_sizes()
+        self.plan = program.plan(dtype, self.level_sizes, self.dims_map)
+        if program.kind == "sddmm":
+            if dense_out is None:
+                dense_out = out.numel() != sp.nnz
+            self.plan.params[7] = 1 if dense_out else 0
+        ws = lib.spx_workspace_size(ctypes.byref(self.plan), self._dims)
+        self.workspace = torch.empty(max(int(ws), 1), dtype=torch.uint8, device=out.device)
+        self.ws_bytes = int(ws)
+        self._lib = lib
+
+    def launch(self, stream: int | None = None) -> None:
+        s = stream if stream is not None else _cur_stream(self.out.device)
+        st = self._lib.spx_launch(
+            ctypes.byref(self.plan),
+            ctypes.c_void_p(self.out.data_ptr()),
+            self._vals,
+            self._pos,
+            self._crd,
+            self._dims,
+            ctypes.c_void_p(self.workspace.data_ptr()),
+            ctypes.c_size_t(self.ws_bytes),
+            ctypes.c_void_p(s),
+        )
+        _lib.check(st, f"spx_launch[{self.program.kernel}]")
+
+    def stats(self) -> "ExecStats":
+        return ExecStats(self.program, self.plan, self.sparse, self.dims_map)
+
+
+def _infer_dtype(inputs: dict) -> str:
+    for v in inputs.values():
+        if isinstance(v, DeviceTensor):
+            if v.dtype == "f32":
+                return "f32"
+        elif isinstance(v, torch.Tensor):
+            if v.dtype == torch.float32:
+                return "f32"
+        elif isinstance(v, np.ndarray) and v.dtype == np.float32:
+            return "f32"
+    return "f64"
+
+
+def _dims_of(x) -> tuple:
+    if isinstance(x, DeviceTensor):
+        return x.dims
+    if isinstance(x, torch.Tensor):
+        return tuple(x.shape)
+    if hasattr(x, "dims"):
+        return tuple(x.dims)
+    return tuple(np.shape(x))
+
+
+def _check_extents(program: Program, inputs: dict) -> dict:
+    """tensors.py:271-289 semantics (DimensionMismatchError on conflict)."""
+    E = _spindle.errors
+    extents: dict[str, int] = {}
+    dims = {}
+    for acc in program.stmt.assignment.input_accesses():
+        if acc.tensor not in inputs:
+            raise E.TensorError(f"tensor {acc.tensor!r} is not bound")
+        d = _dims_of(inputs[acc.tensor])
+        dims[acc.tensor] = d
+        if len(d) != len(acc.vars):
+            raise E.DimensionMismatchError(
+                f"access {acc!r} has {len(acc.vars)} variables but tensor has order {len(d)}")
+        for v, n in zip(acc.vars, d):
+            if v.name in extents and extents[v.name] != n:
+                raise E.DimensionMismatchError(f"variable {v.name!r} used with extents {extents[v.name]} and {n}")
+            extents.setdefault(v.name, int(n))
+    return dims
+
+
+def _check_formats(program: Program, ops: dict) -> None:
+    E = _spindle.errors
+    fmt = _spindle.tensors.format_shorthand
+    for t in program.tensor_order:
+        want = fmt(program.stmt.formats[t])
+        if ops[t].levels != want:
+            raise E.TensorError(f"tensor {t!r} is stored as {ops[t].levels!r} but the statement binds {want!r}")
+
+
+def out_shape(program: Program, dims: dict, sparse_output: bool) -> tuple:
+    if program.kind == "sddmm" and sparse_output:
+        return (-1,)
+    return program.out_dims(dims)
+
+
+def execute(program: Program, operands: dict, out: torch.Tensor, *, stream: int | None = None,
+            dense_out: bool | None = None) -> Executor:
+    """Launch on device-resident operands (no synchronisation, no copies)."""
+    dtype = dtype_name(out.dtype)
+    ex = Executor(program, operands, out, dtype=dtype, dense_out=dense_out)
+    ex.launch(stream)
+    return ex
+
+
+def interpret(program: Program, inputs: dict, out_dims=None, *, dtype: str | None = None, device=None,
+              out: torch.Tensor | None = None, sparse_output: bool | None = None):
+    """Evaluate a lowered statement on the GPU.
+
+    Returns ``(result, ExecStats)``.  ``result`` is a reference
+    `DenseTensor` (fp64) unless `out` is given, in which case the
+    output is written there (host or device torch tensor) and `out` is
+    returned.  An SDDMM whose dense output would exceed DENSE_SDDMM_LIMIT
+    elements (or with ``sparse_output=True``) returns a reference `Tensor` on
+    the sparse operand's pattern instead.
+    """
+    E = _spindle.errors
+    if not torch.cuda.is_available():
+        raise E.ExecutionError("interpret needs a CUDA device (there is no CPU fallback)")
+    _lib.load()
+    device = torch.device(device or "cuda")
+    dtype = dtype or _infer_dtype(inputs)
+    dims = _check_extents(program, inputs)
+    if program.dims is None:
+        program.dims = dims
+    ops = {}
+    fmt = _spindle.tensors.format_shorthand
+    for t in program.tensor_order:
+        ops[t] = as_device_operand(inputs[t], fmt(program.stmt.formats[t]), device, dtype)
+    _check_formats(program, ops)
+    odims = program.out_dims(dims)
+    if out_dims is not None and tuple(out_dims) != tuple(odims):
+        raise E.DimensionMismatchError(f"out_dims {tuple(out_dims)} but the statement produces {odims}")
+    sp = ops[program.ec.tensors[0]]
+    if program.kind == "sddmm":
+        if sparse_output is None:
+            sparse_output = math.prod(odims) > DENSE_SDDMM_LIMIT
+    else:
+        sparse_output = False
+    n_out = sp.nnz if sparse_output else math.prod(odims)
+    td = torch_dtype(dtype)
+    if out is not None and out.device.type == "cuda":
+        dev_out = out
+    else:
+        dev_out = torch.empty(n_out, dtype=td, device=device)
+    if dev_out.numel() != n_out:
+        raise E.DimensionMismatchError(f"output buffer has {dev_out.numel()} elements, need {n_out}")
+    ex = Executor(program, ops, dev_out, dtype=dtype, dense_out=not sparse_output)
+    ex.launch()
+    stats = ex.stats()
+    if out is not None:
+        if out.device.type != "cuda":
+            out.copy_(dev_out.view_as(out), non_blocking=True)
+        torch.cuda.current_stream(device).synchronize()
+        return out, stats
+    host = dev_out.cpu().numpy().astype(np.float64)
+    T = _spindle.tensors
+    if sparse_output:
+        ref = sp.to_reference()
+        ref.vals = host
+        return ref, stats
+    return T.DenseTensor(tuple(odims), host.reshape(odims)), stats
+
+
+# ---------------------------------------------------------------------------
+# ExecStats
+# ---------------------------------------------------------------------------
+
+
+def _chunks(total: int, size: int) -> np.ndarray:
+    if total <= 0 or size <= 0:
+        return np.zeros(0, dtype=np.int64)
+    n = -(-total // size)
+    w = np.full(n, size, dtype=np.int64)
+    w[-1] = total - size * (n - 1)
+    return w
+
+
+def _segment_sums(pos: np.ndarray, seg_per_chunk: int) -> np.ndarray:
+    """Leaf positions per chunk of `seg_per_chunk` consecutive segments."""
+    nseg = len(pos) - 1
+    if nseg <= 0:
+        return np.zeros(0, dtype=np.int64)
+    starts = np.arange(0, nseg, seg_per_chunk)
+    ends = np.minimum(starts + seg_per_chunk, nseg)
+    p = pos.astype(np.int64)
+    return p[ends] - p[starts]
+
+
+class ExecStats:
+    """Work counts of one execution, computed exactly from the partition
+    (per-loop iteration counts, per-parallel-instance work,
+    guard failures; sum of per-instance work == total innermost work)."""
+
+    def __init__(self, program: Program, plan, sparse: DeviceTensor, dims: dict):
+        self.program = program
+        self.kernel = program.kernel
+        self.params = [int(plan.params[k]) for k in range(8)]
+        self._sparse = sparse
+        self._dims = dims
+
+    def _pos(self, lvl: int) -> np.ndarray:
+        return self._sparse.pos[lvl].cpu().numpy()
+
+    @cached_property
+    def _computed(self):
+        prog, p = self.program, self.params
+        sp = self._sparse
+        sizes = sp.level_sizes()
+        nnz = sizes[-1]
+        v = prog.vars
+        inst: dict[str, np.ndarray] = {}
+        loops: dict[str, int] = {}
+        guards: dict[str, int] = {}
+        kid = prog.kernel_id
+        if kid in (_lib.K_SPMV_NNZ, _lib.K_SPMM_NNZ, _lib.K_SDDMM_NNZ, _lib.K_MTTKRP_NNZ):
+            TB, W = p[0], p[1]
+            blocks = _chunks(nnz, TB)
+            warps = np.concatenate([_chunks(int(b), W) for b in blocks]) if len(blocks) else blocks
+            inst[v["block"]] = blocks
+            inst[v["warp"]] = warps
+            loops[v["block"]] = len(blocks)
+            loops[v["warp"]] = len(warps)
+            guards[v["block"]] = len(blocks) * TB - nnz
+            if kid == _lib.K_SPMV_NNZ:
+                T = p[2]
+                threads = np.concatenate([_chunks(int(w), T) for w in warps]) if len(warps) else warps
+                inst[v["thread"]] = threads
+                loops[v["thread"]] = len(threads)
+        elif kid in (_lib.K_SPMV_ROW, _lib.K_SPMV_WARP, _lib.K_SPMM_ROW, _lib.K_SDDMM_ROW):
+            pos = self._pos(1)
+            R = max(1, p[0])
+            rows = len(pos) - 1
+            blk = _segment_sums(pos, R)
+            name = v.get("block") or "block"
+            inst[name] = blk
+            loops[name] = len(blk)
+            guards[name] = len(blk) * R - rows
+            per_row = np.diff(pos.astype(np.int64))
+            inner = v.get("thread") if kid == _lib.K_SPMV_ROW else v.get("warp")
+            if inner:
+                inst[inner] = per_row
+        elif kid == _lib.K_TTV_FIBER:
+            pos2 = self._pos(2)
+            FTB, FW = max(1, p[0]), max(1, p[1])
+            name = v.get("block") or "block"
+            inst[name] = _segment_sums(pos2, FTB)
+            loops[name] = len(inst[name])
+            if v.get("warp"):
+                inst[v["warp"]] = _segment_sums(pos2, FW)
+        elif kid == _lib.K_MTTKRP_SLICE:
+            pos1, pos2 = self._pos(1), self._pos(2)
+            slice_leaves = pos2[pos1.astype(np.int64)].astype(np.int64)
+            CH = max(1, p[0])
+            name = v.get("block") or "block"
+            inst[name] = _segment_sums(slice_leaves, CH)
+            loops[name] = len(inst[name])
+            if v.get("warp"):
+                inst[v["warp"]] = np.diff(slice_leaves)
+        return inst, loops, guards
+
+    @property
+    def instance_work(self) -> dict:
+        return self._computed[0]
+
+    @property
+    def loop_counts(self) -> dict:
+        return self._computed[1]
+
+    @property
+    def guard_failures(self) -> dict:
+        return self._computed[2]
+
+    def work(self, var: str) -> np.ndarray:
+        return self.instance_work[var]
+
+    def summary(self) -> dict:
+        out = {"kernel": self.kernel, "params": self.params[:4]}
+        for k, w in self.instance_work.items():
+            if len(w):
+                out[k] = {"n": int(len(w)), "min": int(w.min()), "max": int(w.max()), "mean": float(w.mean()),
+                          "sum": int(w.sum())}
+        return out
