@@ -33,6 +33,51 @@ template <typename T>
 __device__ __forceinline__ void st_stream(T* p, T v) { __stcs(p, v); }
 
 // ---------------------------------------------------------------------------
+// L2 residency control (createpolicy + .L2::cache_hint).  The gathered dense
+// operand is tagged evict_last so that the streamed sparse arrays and the
+// output (tagged evict_first) do not push its hot rows out of the 126 MB L2.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t l2_evict_last() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_evict_first() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ float4 ld_f4_hint(const void* p, uint64_t pol) {
+  float4 r;
+  asm("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+      : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+      : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ void st_f4_hint(void* p, float4 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ int ld_i32_first(const int32_t* p, uint64_t pol) {
+  int r;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ float ld_f32_first(const float* p, uint64_t pol) {
+  float r;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r) : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ double ld_f64_first(const double* p, uint64_t pol) {
+  double r;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ float ld_stream_hint(const float* p, uint64_t pol) { return ld_f32_first(p, pol); }
+__device__ __forceinline__ double ld_stream_hint(const double* p, uint64_t pol) { return ld_f64_first(p, pol); }
+
+// ---------------------------------------------------------------------------
 // Per-lane row fragments: a lane owns VPL values of a dense row.
 // CONTIG: lane owns columns [lane*VPL, lane*VPL+VPL) -> vector loads.
 // !CONTIG: lane owns columns {v*32 + lane} (the literal `split(k, dv,
@@ -73,6 +118,34 @@ struct Frag {
         int k = i * 32 + lane;
         v[i] = k < ncols ? __ldg(row + k) : T(0);
       }
+    }
+  }
+
+  // gather with an L2 eviction-priority policy (16 B vector path)
+  __device__ __forceinline__ void load_hint(const T* __restrict__ row, int lane, int ncols, uint64_t pol) {
+    constexpr int BYTES = VPL * (int)sizeof(T);
+    if constexpr (CONTIG && BYTES % 16 == 0) {
+      const T* p = row + lane * VPL;
+#pragma unroll
+      for (int c = 0; c < BYTES / 16; ++c) {
+        float4 q = ld_f4_hint(reinterpret_cast<const float4*>(p) + c, pol);
+        *reinterpret_cast<float4*>(&v[c * (16 / sizeof(T))]) = q;
+      }
+    } else {
+      load(row, lane, ncols);
+    }
+  }
+
+  __device__ __forceinline__ void store_hint(T* __restrict__ row, int lane, int ncols, uint64_t pol) const {
+    constexpr int BYTES = VPL * (int)sizeof(T);
+    if constexpr (CONTIG && BYTES % 16 == 0) {
+      T* p = row + lane * VPL;
+#pragma unroll
+      for (int c = 0; c < BYTES / 16; ++c)
+        st_f4_hint(reinterpret_cast<float4*>(p) + c, *reinterpret_cast<const float4*>(&v[c * (16 / sizeof(T))]),
+                   pol);
+    } else {
+      store(row, lane, ncols);
     }
   }
 

@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(kMaxThreads) sddmm_row_kernel(const int32_t* _
 template <typename T, int VPL, bool CONTIG>
 int run_sddmm(int kid, const Args& a) {
   constexpr int words = VPL * (int)sizeof(T) / 4;
-  constexpr int U = words >= 8 ? 4 : 8;
+  constexpr int U = words >= 16 ? 2 : (words >= 8 ? 4 : 8);
   const int32_t* pos = a.pos[0];
   const int32_t* crd = a.crd[0];
   const T* vals = static_cast<const T*>(a.vals[0]);
@@ -194,7 +194,7 @@ int run_sddmm(int kid, const Args& a) {
 
 template <typename T>
 int dispatch_sddmm(int kid, const Args& a, int64_t K) {
-  const int vmax = sizeof(T) == 4 ? 8 : 4;
+  const int vmax = 8;
   int v = (int)ceil_div(K < 1 ? 1 : K, 32), vpl = 1;
   while (vpl < v) vpl <<= 1;
   if (vpl > vmax)
@@ -209,9 +209,7 @@ int dispatch_sddmm(int kid, const Args& a, int64_t K) {
     case 9: return run_sddmm<T, 4, true>(kid, a);
     default: break;
   }
-  if constexpr (sizeof(T) == 4) {
-    if (vpl == 8) return contig ? run_sddmm<T, 8, true>(kid, a) : run_sddmm<T, 8, false>(kid, a);
-  }
+  if (vpl == 8) return contig ? run_sddmm<T, 8, true>(kid, a) : run_sddmm<T, 8, false>(kid, a);
   return fail(SPX_E_UNSUPPORTED, "no SDDMM instantiation");
 }
 

@@ -102,54 +102,86 @@ __global__ void __launch_bounds__(kMaxThreads) spmm_nnz_kernel(
       int64_t lb = warp_lower_bound(pos, 0, r, q0, lane);
       for (int64_t rr = lb; rr < r; ++rr) store_zero_row<T, VPL, CONTIG>(Cp + rr * N, lane, ncols);
     }
+    // Hot loop.  Positions fit int32 (pos is int32, tensors.py:248).  The
+    // next 32 (crd, vals) are fetched one batch ahead; within a batch the B
+    // gathers run two groups of U rows ahead of the FMAs (double buffer),
+    // so each warp keeps up to 2*U 512 B rows in flight.
+    const uint64_t pol_b = l2_evict_last();
+    const uint64_t pol_s = l2_evict_first();
     RowEndCache ends;
     ends.fill(pos, r, M, lane);
-    int64_t rend = ends.end(pos, r, M, lane);
+    int rr32 = (int)r;
+    int rend = (int)ends.end(pos, r, M, lane);
     F acc;
     acc.zero();
-    for (int64_t p = q0; p < q1; p += 32) {
-      const int n = (int)min((int64_t)32, q1 - p);
-      int my_c = 0;
-      T my_v = T(0);
-      if (lane < n) {
-        my_c = __ldcs(crd + p + lane);
-        my_v = __ldcs(vals + p + lane);
+    const int qe = (int)q1;
+    int p = (int)q0;
+    int nc = 0;
+    T nv = T(0);
+    if (p + lane < qe) {
+      nc = ld_i32_first(crd + p + lane, pol_s);
+      nv = ld_stream_hint(vals + p + lane, pol_s);
+    }
+    auto flush = [&]() {
+      if (is_head) {
+        acc.store_smem(sval + warp * PW, lane);
+        head = rr32;
+        is_head = false;
+      } else {
+        acc.store_hint(Cp + (int64_t)rr32 * N, lane, ncols, pol_s);
       }
-      for (int t0 = 0; t0 < n; t0 += U) {
-        F b[U];
+      acc.zero();
+    };
+    constexpr int G = 32 / U;
+    while (p < qe) {
+      const int n = min(32, qe - p);
+      const int my_c = nc;
+      const T my_v = nv;
+      if (p + 32 + lane < qe) {
+        nc = ld_i32_first(crd + p + 32 + lane, pol_s);
+        nv = ld_stream_hint(vals + p + 32 + lane, pol_s);
+      }
+      F buf0[U], buf1[U];
+      auto gather = [&](F(&buf)[U], int g) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const int c = __shfl_sync(kFull, my_c, (t0 + u) & 31);
-          if (t0 + u < n) b[u].load(Bp + (int64_t)c * N, lane, ncols);
+          const int c = __shfl_sync(kFull, my_c, (g * U + u) & 31);
+          if (g * U + u < n) buf[u].load_hint(Bp + (int64_t)c * N, lane, ncols, pol_b);
         }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          if (t0 + u < n) {
-            const T v = __shfl_sync(kFull, my_v, (t0 + u) & 31);
-            const int64_t pp = p + t0 + u;
-            while (pp >= rend) {
-              if (is_head) {
-                acc.store_smem(sval + warp * PW, lane);
-                head = (int32_t)r;
-                is_head = false;
-              } else {
-                acc.store(Cp + r * N, lane, ncols);
-              }
-              acc.zero();
-              ++r;
-              rend = ends.end(pos, r, M, lane);
-            }
-            acc.fma(v, b[u]);
+      };
+      auto consume = [&](F(&buf)[U], int g) {
+        const int base = p + g * U;
+        const int cnt = min(U, n - g * U);
+        int u0 = 0;
+        while (true) {
+          while (base + u0 >= rend) {  // row(s) finished: store, skip empty rows
+            flush();
+            ++rr32;
+            rend = (int)ends.end(pos, rr32, M, lane);
           }
+          const int stop = min(cnt, rend - base);
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const T v = __shfl_sync(kFull, my_v, (g * U + u) & 31);
+            if (u >= u0 && u < stop) acc.fma(v, buf[u]);
+          }
+          u0 = stop;
+          if (u0 >= cnt) break;
         }
+      };
+      gather(buf0, 0);
+      for (int g = 0; g < G; g += 2) {
+        if (g * U >= n) break;
+        if ((g + 1) * U < n) gather(buf1, g + 1);
+        consume(buf0, g);
+        if ((g + 1) * U >= n) break;
+        if (g + 2 < G && (g + 2) * U < n) gather(buf0, g + 2);
+        consume(buf1, g + 1);
       }
+      p += n;
     }
-    if (is_head) {
-      acc.store_smem(sval + warp * PW, lane);
-      head = (int32_t)r;
-    } else {
-      acc.store(Cp + r * N, lane, ncols);
-    }
+    flush();
+    r = rr32;
     if (q1 == nnz) {
       // trailing rows with pos[r] == nnz belong to the last chunk
       for (int64_t rr = r + 1; rr < M; ++rr) store_zero_row<T, VPL, CONTIG>(Cp + rr * N, lane, ncols);

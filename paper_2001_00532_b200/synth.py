@@ -19,7 +19,7 @@ Coordinate draws come in batches of BATCH=2^22, batch b from
 `default_rng([seed, b])` (so they run on all host cores); the subset choice,
 permutations and values come from `default_rng(seed)`.
 
-Results are cached as .npz under $SPX_CACHE (default <repo>/.cache/synth,
+Results are cached as .npz under $SPX_CACHE (default ~/.cache/spx_synth, outside the repo
 git- and gpurun-ignored).
 """
 
@@ -32,7 +32,7 @@ from pathlib import Path
 
 import numpy as np
 
-CACHE = Path(os.environ.get("SPX_CACHE", Path(__file__).resolve().parent.parent / ".cache" / "synth"))
+CACHE = Path(os.environ.get("SPX_CACHE", Path.home() / ".cache" / "spx_synth"))
 
 
 @dataclass

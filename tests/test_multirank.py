@@ -1,0 +1,73 @@
+"""The N>1 host path on CPU: world_size-2 gloo process groups over 127.0.0.1.
+
+Each rank takes its nnz-balanced shard from the partitioner, computes its
+disjoint output rows (here with the CPU oracle standing in for the GPU
+kernel -- test-only), and the shards are combined with the same collectives
+the GPU path uses: `gather_rows` (SpMM/SpMV/SDDMM) and `reduce_partials`
+(MTTKRP with slices split across ranks).
+"""
+
+from __future__ import annotations
+
+import os
+import socket
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+import torch.multiprocessing as mp
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank: int, world: int, port: int, q):
+    sys.path.insert(0, str(ROOT))
+    import torch.distributed as dist
+
+    from oracle import oracle as O
+    from paper_2001_00532_b200 import synth
+    from paper_2001_00532_b200.partition import csf_shards, csr_shards, gather_rows, reduce_partials
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        A = synth.rmat_csr(10, 20_000, seed=5, cache=False)
+        B = synth.dense((A.N, 16), seed=6)
+        shards = csr_shards(A.pos, A.crd, A.vals, world)
+        s = shards[rank]
+        local = torch.from_numpy(O.spmm(s.pos, s.crd, s.vals, B))
+        full = gather_rows(local, [x.row1 - x.row0 for x in shards]).numpy()
+        ok_spmm = np.allclose(full, O.spmm(A.pos, A.crd, A.vals, B), rtol=1e-12, atol=1e-12)
+
+        T = synth.bitskew_csf(6, 5000, seed=7, cache=False)
+        C = synth.dense((64, 8), seed=8)
+        D = synth.dense((64, 8), seed=9)
+        part = csf_shards(T.pos, T.crd, T.vals, world, exact=True)[rank]
+        partial = torch.from_numpy(O.mttkrp(T.dims, part.pos, part.crd, part.vals, C, D))
+        tot = reduce_partials(partial).numpy()
+        ok_mttkrp = np.allclose(tot, O.mttkrp(T.dims, T.pos, T.crd, T.vals, C, D), rtol=1e-10, atol=1e-12)
+        q.put((rank, bool(ok_spmm), bool(ok_mttkrp)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_gloo_shards_and_collectives():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+    res = sorted(q.get(timeout=5) for _ in range(2))
+    assert res == [(0, True, True), (1, True, True)]
+    assert all(p.exitcode == 0 for p in procs)

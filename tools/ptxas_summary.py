@@ -9,7 +9,7 @@ for ln in lines:
     m = re.search(r"Compiling entry function '([^']+)'", ln)
     if m:
         name = m.group(1)
-        k = re.search(r"\d+([a-z_]+kernel)(I[^E]*E)?", name)
+        k = re.search(r"\d+([a-z_]+kernel)(I.*?EEv)?", name)
         cur = (k.group(1) + (k.group(2) or "")) if k else name[:60]
         continue
     m = re.search(r"Used (\d+) registers.*?(?:(\d+) bytes cumulative stack size)?", ln)
