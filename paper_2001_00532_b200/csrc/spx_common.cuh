@@ -77,6 +77,18 @@ __device__ __forceinline__ double ld_f64_first(const double* p, uint64_t pol) {
 __device__ __forceinline__ float ld_stream_hint(const float* p, uint64_t pol) { return ld_f32_first(p, pol); }
 __device__ __forceinline__ double ld_stream_hint(const double* p, uint64_t pol) { return ld_f64_first(p, pol); }
 
+// cp.async (LDGSTS) 16 B global -> shared, L1 bypass, with an L2 policy.
+__device__ __forceinline__ void cp_async16(uint32_t smem_addr, const void* gptr, uint64_t pol) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_addr), "l"(gptr),
+               "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // ---------------------------------------------------------------------------
 // Per-lane row fragments: a lane owns VPL values of a dense row.
 // CONTIG: lane owns columns [lane*VPL, lane*VPL+VPL) -> vector loads.
@@ -206,6 +218,19 @@ struct Frag {
   }
 
   __device__ __forceinline__ void fma(T s, const Frag& b) {
+#if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 1000
+    if constexpr (sizeof(T) == 4 && VPL % 2 == 0) {
+      // packed FFMA2: half the issue slots of scalar FFMA, same rounding
+      const float2 ss = make_float2(s, s);
+#pragma unroll
+      for (int i = 0; i < VPL; i += 2) {
+        const float2 r = __ffma2_rn(ss, make_float2(b.v[i], b.v[i + 1]), make_float2(v[i], v[i + 1]));
+        v[i] = r.x;
+        v[i + 1] = r.y;
+      }
+      return;
+    }
+#endif
 #pragma unroll
     for (int i = 0; i < VPL; ++i) v[i] = s * b.v[i] + v[i];
   }

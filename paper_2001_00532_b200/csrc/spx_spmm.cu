@@ -27,6 +27,8 @@
 //    warp-per-row schedule): split(i,block,block_row,ROWS_PER_TB)
 //    split(block_row,warp_row,warp,WARPS) -> warp w of block b handles rows
 //    b*ROWS + warp_row*WARPS + w; lanes cover k.
+#include <cstdlib>
+
 #include "spx_common.cuh"
 
 namespace spx {
@@ -69,17 +71,42 @@ __device__ __forceinline__ void store_zero_row(T* __restrict__ row, int lane, in
   z.store(row, lane, ncols);
 }
 
-template <typename T, int VPL, bool CONTIG, int U>
+// One batch of 32 consecutive positions held one per lane: column (with the
+// hot-row flag in bit 31, see spx_spmm_analyze) and value.
+template <typename T>
+struct Batch {
+  int c;
+  T v;
+  __device__ __forceinline__ void load(const int32_t* __restrict__ crd, const T* __restrict__ vals, int idx, int end,
+                                       const uint32_t* __restrict__ hot, uint64_t pol) {
+    c = 0;
+    v = T(0);
+    if (idx < end) {
+      c = ld_i32_first(crd + idx, pol);
+      v = ld_stream_hint(vals + idx, pol);
+      if (hot && ((__ldg(hot + (c >> 5)) >> (c & 31)) & 1u)) c |= int(0x80000000u);
+    }
+  }
+};
+
+// RING == 0: register double-buffered gathers (any VPL / mapping).
+// RING  > 0: cp.async ring of RING row slots per warp in shared memory
+//            (CONTIG rows of 16 or 32 B per lane): each lane copies and later
+//            reads back only its own 16 B pieces, so the per-lane
+//            cp.async.wait_group is the only synchronisation; no data
+//            registers are held for rows in flight, which buys occupancy.
+template <typename T, int VPL, bool CONTIG, int U, int RING>
 __global__ void __launch_bounds__(kMaxThreads) spmm_nnz_kernel(
     const int32_t* __restrict__ pos, const int32_t* __restrict__ crd, const T* __restrict__ vals,
     const T* __restrict__ B, T* __restrict__ C, int64_t M, int64_t N, int64_t nnz, int64_t TB,
-    int64_t W, int32_t* __restrict__ carry_row, T* __restrict__ carry_val) {
+    int64_t W, int32_t* __restrict__ carry_row, T* __restrict__ carry_val, const uint32_t* __restrict__ hot) {
   using F = Frag<T, VPL, CONTIG>;
   constexpr int PW = 32 * VPL;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int nw = blockDim.x >> 5;
   T* sval = reinterpret_cast<T*>(smem_raw);
   int32_t* srow = reinterpret_cast<int32_t*>(sval + nw * PW);
+  T* ring_base = reinterpret_cast<T*>(smem_raw + ((nw * (PW * sizeof(T) + sizeof(int32_t)) + 15) & ~size_t(15)));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t cta = blockIdx.x, ncta = gridDim.x;
@@ -116,12 +143,6 @@ __global__ void __launch_bounds__(kMaxThreads) spmm_nnz_kernel(
     acc.zero();
     const int qe = (int)q1;
     int p = (int)q0;
-    int nc = 0;
-    T nv = T(0);
-    if (p + lane < qe) {
-      nc = ld_i32_first(crd + p + lane, pol_s);
-      nv = ld_stream_hint(vals + p + lane, pol_s);
-    }
     auto flush = [&]() {
       if (is_head) {
         acc.store_smem(sval + warp * PW, lane);
@@ -132,6 +153,89 @@ __global__ void __launch_bounds__(kMaxThreads) spmm_nnz_kernel(
       }
       acc.zero();
     };
+    if constexpr (RING > 0) {
+      static_assert(CONTIG && (VPL * sizeof(T)) % 16 == 0, "ring path needs 16 B lane pieces");
+      static_assert(32 % RING == 0 && RING % 4 == 0, "ring depth must divide the 32-position batch");
+      constexpr int LB = VPL * (int)sizeof(T);  // bytes per lane per row
+      constexpr int ROWB = 32 * LB;
+      constexpr int GS = 4;          // positions per cp.async commit group
+      constexpr int NG = RING / GS;  // groups resident in the ring
+      T* ring = ring_base + (size_t)warp * RING * PW;
+      const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring) + lane * LB;
+      const T* ring_lane = ring + lane * VPL;
+      const char* Bb = reinterpret_cast<const char*>(Bp) + lane * LB;
+      const uint32_t rowstride = (uint32_t)(N * (int64_t)sizeof(T));
+      const int n = qe - p;
+      Batch<T> b0, b1, b2;  // batches k, k+1 (resident) and k+2 (in flight)
+      b0.load(crd, vals, p + lane, qe, nullptr, pol_s);
+      b1.load(crd, vals, p + 32 + lane, qe, nullptr, pol_s);
+      b2.load(crd, vals, p + 64 + lane, qe, nullptr, pol_s);
+      auto issue = [&](int c, int slot) {
+        const char* src = Bb + (uint64_t)(uint32_t)c * rowstride;
+#pragma unroll
+        for (int k = 0; k < LB / 16; ++k) cp_async16(ring_s + slot * ROWB + k * 16, src + k * 16, pol_b);
+      };
+      // prologue: groups 0 .. NG-2 in flight
+#pragma unroll
+      for (int t = 0; t < RING - GS; ++t) {
+        const int c = __shfl_sync(kFull, b0.c, t);
+        if (t < n) issue(c, t);
+        if (t % GS == GS - 1) cp_async_commit();
+      }
+      for (int base = 0; base < n; base += 32) {
+        const bool full = base + 32 + RING - GS <= n;
+#pragma unroll
+        for (int j = 0; j < 32 / GS; ++j) {
+          // issue group j+NG-1 (may reach into the next batch)
+#pragma unroll
+          for (int u = 0; u < GS; ++u) {
+            const int t = (j + NG - 1) * GS + u;
+            const int c = __shfl_sync(kFull, t < 32 ? b0.c : b1.c, t & 31);
+            if (full || base + t < n) issue(c, t % RING);
+          }
+          cp_async_commit();
+          cp_async_wait<NG - 1>();  // group j has landed (for this lane's pieces)
+          if (!full && base + j * GS >= n) break;
+          const int gbase = p + base + j * GS;
+          const int cnt = full ? GS : min(GS, n - base - j * GS);
+          T vv[GS];
+          F bv[GS];
+#pragma unroll
+          for (int u = 0; u < GS; ++u) {
+            vv[u] = __shfl_sync(kFull, b0.v, j * GS + u);
+            const float4* sp = reinterpret_cast<const float4*>(ring_lane + ((j * GS + u) % RING) * PW);
+#pragma unroll
+            for (int k = 0; k < LB / 16; ++k) *reinterpret_cast<float4*>(&bv[u].v[k * (16 / sizeof(T))]) = sp[k];
+          }
+          if (cnt == GS && gbase + GS <= rend) {
+#pragma unroll
+            for (int u = 0; u < GS; ++u) acc.fma(vv[u], bv[u]);
+          } else {
+#pragma unroll
+            for (int u = 0; u < GS; ++u) {
+              if (u < cnt) {
+                while (gbase + u >= rend) {  // row(s) finished: store, skip empty rows
+                  flush();
+                  ++rr32;
+                  rend = (int)ends.end(pos, rr32, M, lane);
+                }
+                acc.fma(vv[u], bv[u]);
+              }
+            }
+          }
+        }
+        b0 = b1;
+        b1 = b2;
+        b2.load(crd, vals, p + base + 96 + lane, qe, nullptr, pol_s);
+      }
+      cp_async_wait<0>();
+    } else {
+    int nc = 0;
+    T nv = T(0);
+    if (p + lane < qe) {
+      nc = ld_i32_first(crd + p + lane, pol_s);
+      nv = ld_stream_hint(vals + p + lane, pol_s);
+    }
     constexpr int G = 32 / U;
     while (p < qe) {
       const int n = min(32, qe - p);
@@ -180,6 +284,7 @@ __global__ void __launch_bounds__(kMaxThreads) spmm_nnz_kernel(
       }
       p += n;
     }
+    }  // RING == 0
     flush();
     r = rr32;
     if (q1 == nnz) {
@@ -315,6 +420,16 @@ int check_bound(const Args& a, int64_t N) {
   return SPX_OK;
 }
 
+// Depth of the cp.async row ring (0 = register pipeline); SPX_SPMM_RING
+// overrides the default for tuning sweeps.
+int ring_depth() {
+  static const int d = [] {
+    const char* s = getenv("SPX_SPMM_RING");
+    return s ? atoi(s) : 8;
+  }();
+  return d;
+}
+
 template <typename T, int VPL, bool CONTIG>
 int run_spmm(int kid, const Args& a, const SpmmGeom& g) {
   constexpr int U = unroll_for<T, VPL>();
@@ -340,10 +455,31 @@ int run_spmm(int kid, const Args& a, const SpmmGeom& g) {
     T* carry_val = static_cast<T*>(a.ws);
     int32_t* carry_row = reinterpret_cast<int32_t*>(
         reinterpret_cast<char*>(a.ws) + (((size_t)ncta * g.npanels * g.pw * sizeof(T) + 255) & ~(size_t)255));
-    const size_t smem = (size_t)nw * (g.pw * sizeof(T) + sizeof(int32_t));
+    const size_t head_smem = ((size_t)nw * (g.pw * sizeof(T) + sizeof(int32_t)) + 15) & ~size_t(15);
     dim3 grid((unsigned)ncta, (unsigned)g.npanels);
-    spmm_nnz_kernel<T, VPL, CONTIG, U><<<grid, nw * 32, smem, a.stream>>>(pos, crd, vals, B, C, M, N, nnz, TB,
-                                                                          W, carry_row, carry_val);
+    const uint32_t* hot = nullptr;
+    const int ring = ring_depth();
+    if constexpr (CONTIG && (VPL * sizeof(T)) % 16 == 0) {
+      if (ring > 0) {
+        auto launch = [&](auto kern, int depth) -> int {
+          const size_t smem = head_smem + (size_t)nw * depth * g.pw * sizeof(T);
+          if (int e = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                                 "cudaFuncSetAttribute"))
+            return e;
+          kern<<<grid, nw * 32, smem, a.stream>>>(pos, crd, vals, B, C, M, N, nnz, TB, W, carry_row, carry_val, hot);
+          return SPX_OK;
+        };
+        int e = ring >= 16 ? launch(spmm_nnz_kernel<T, VPL, CONTIG, U, 16>, 16)
+                           : launch(spmm_nnz_kernel<T, VPL, CONTIG, U, 8>, 8);
+        if (e) return e;
+      } else {
+        spmm_nnz_kernel<T, VPL, CONTIG, U, 0><<<grid, nw * 32, head_smem, a.stream>>>(
+            pos, crd, vals, B, C, M, N, nnz, TB, W, carry_row, carry_val, hot);
+      }
+    } else {
+      spmm_nnz_kernel<T, VPL, CONTIG, U, 0><<<grid, nw * 32, head_smem, a.stream>>>(
+          pos, crd, vals, B, C, M, N, nnz, TB, W, carry_row, carry_val, hot);
+    }
     count_launch();
     if (int e = check_cuda(cudaGetLastError(), "spmm_nnz_kernel")) return e;
     const int fw = 8;

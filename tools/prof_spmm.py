@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--nnz", type=int, default=50_000_000)
     ap.add_argument("--iters", type=int, default=4)
     ap.add_argument("--kind", default="spmm", choices=["spmm", "spmv", "sddmm", "mttkrp"])
+    ap.add_argument("--gather", action="store_true")
     a = ap.parse_args()
     dev = torch.device("cuda:0")
     if a.kind == "spmm":
@@ -48,5 +49,28 @@ def main():
     print("done")
 
 
+
+
+def gather_only():
+    """Also launch the gather microbenchmark on the same column stream."""
+    import ctypes
+    sys.path.insert(0, str(ROOT / "tools"))
+    import gbench
+
+    lib = gbench.build()
+    A = synth.rmat_csr(20, 50_000_000, seed=2)
+    dev = torch.device("cuda:0")
+    cols = torch.from_numpy(A.crd).to(dev)
+    B = torch.rand(A.N, 128, device=dev)
+    out = torch.empty(((A.nnz + 255) // 256 + 1) * 32 * 4 * 4, dtype=torch.float32, device=dev)
+    for _ in range(3):
+        lib.gbench_gather(cols.data_ptr(), A.nnz, B.data_ptr(), 128, out.data_ptr(), 256, 0, 8,
+                          torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+
+
 if __name__ == "__main__":
-    main()
+    if "--gather" in sys.argv:
+        gather_only()
+    else:
+        main()
