@@ -154,6 +154,11 @@ int spx_partition(const int32_t* seg_start, int64_t nseg, int64_t nnz,
 int spx_partition_device(const int32_t* seg_start, int64_t nseg, int64_t nnz,
                          int32_t ndev, int64_t* bounds_out, void* stream);
 
+/* Device self-test: writes the createpolicy.fractional L2::evict_last /
+ * evict_first descriptors of this GPU and the constants the kernels use in
+ * their place (DEVICE uint64_t[4]).  Parity tests require them equal. */
+int spx_selftest(uint64_t* out4, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

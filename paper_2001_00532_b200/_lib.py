@@ -60,6 +60,7 @@ EXPORTS = (
     "spx_launch_count",
     "spx_partition",
     "spx_partition_device",
+    "spx_selftest",
 )
 
 
@@ -115,6 +116,8 @@ def load(path: str | os.PathLike | None = None):
     lib.spx_partition.restype = ctypes.c_int
     lib.spx_partition_device.argtypes = [vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, vp, vp]
     lib.spx_partition_device.restype = ctypes.c_int
+    lib.spx_selftest.argtypes = [vp, vp]
+    lib.spx_selftest.restype = ctypes.c_int
     if path is None:
         _lib = lib
     return lib

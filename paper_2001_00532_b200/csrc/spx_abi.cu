@@ -193,3 +193,19 @@ int spx_partition_device(const int32_t* seg_start, int64_t nseg, int64_t nnz, in
 }
 
 }  // extern "C"
+
+namespace spx {
+__global__ void policy_probe_kernel(uint64_t* out) {
+  out[0] = createpolicy_evict_last();
+  out[1] = createpolicy_evict_first();
+  out[2] = kPolicyEvictLast;
+  out[3] = kPolicyEvictFirst;
+}
+}  // namespace spx
+
+extern "C" int spx_selftest(uint64_t* out4, void* stream) {
+  if (!out4) return spx::fail(SPX_E_ARG, "null output");
+  spx::policy_probe_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(out4);
+  spx::count_launch();
+  return spx::check_cuda(cudaGetLastError(), "policy_probe_kernel");
+}

@@ -37,14 +37,24 @@ __device__ __forceinline__ void st_stream(T* p, T v) { __stcs(p, v); }
 // operand is tagged evict_last so that the streamed sparse arrays and the
 // output (tagged evict_first) do not push its hot rows out of the 126 MB L2.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ uint64_t l2_evict_last() {
+// The 64-bit cache-policy descriptors createpolicy.fractional.L2::evict_*
+// 1.0 produces (the constants CUTLASS uses for its TMA/LDG hints).  Using
+// immediates lets ptxas keep the policy in a uniform register instead of
+// re-deriving it (R2UR) at every cp.async; tests/test_gpu_kernels.py checks
+// they equal what createpolicy returns on the device.
+constexpr uint64_t kPolicyEvictNormal = 0x1000000000000000ull;
+constexpr uint64_t kPolicyEvictFirst = 0x12F0000000000000ull;
+constexpr uint64_t kPolicyEvictLast = 0x14F0000000000000ull;
+__device__ __forceinline__ uint64_t l2_evict_last() { return kPolicyEvictLast; }
+__device__ __forceinline__ uint64_t l2_evict_first() { return kPolicyEvictFirst; }
+__device__ __forceinline__ uint64_t createpolicy_evict_last() {
   uint64_t p;
-  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
-__device__ __forceinline__ uint64_t l2_evict_first() {
+__device__ __forceinline__ uint64_t createpolicy_evict_first() {
   uint64_t p;
-  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
 __device__ __forceinline__ float4 ld_f4_hint(const void* p, uint64_t pol) {
@@ -228,11 +238,12 @@ struct Frag {
         v[i] = r.x;
         v[i + 1] = r.y;
       }
-      return;
-    }
+    } else
 #endif
+    {
 #pragma unroll
-    for (int i = 0; i < VPL; ++i) v[i] = s * b.v[i] + v[i];
+      for (int i = 0; i < VPL; ++i) v[i] = s * b.v[i] + v[i];
+    }
   }
 };
 

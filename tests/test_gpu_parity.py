@@ -153,3 +153,18 @@ def test_device_resident_inputs(cuda):
     got, _ = interpret(prog, dev, out=out)
     assert got is out
     assert rel_err(out.cpu().numpy().reshape(-1, 128), case["result"]) <= 1e-3
+
+
+def test_l2_policy_constants_match_createpolicy(cuda):
+    """The kernels use immediate L2 policy descriptors in place of
+    createpolicy; they must be what createpolicy produces on this GPU."""
+    import ctypes
+
+    from paper_2001_00532_b200 import _lib
+
+    out = torch.zeros(4, dtype=torch.int64, device="cuda")
+    st = _lib.load().spx_selftest(ctypes.c_void_p(out.data_ptr()),
+                                  ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    _lib.check(st)
+    v = [int(x) & 0xFFFFFFFFFFFFFFFF for x in out.cpu().tolist()]
+    assert v[0] == v[2] and v[1] == v[3], [hex(x) for x in v]
