@@ -73,10 +73,7 @@ int resolve(const spx_plan* plan, const void* const* vals, const int32_t* const*
       a->dims[r][d] = dims[off + d];
     }
     off += fam->order[r];
-    if (vals) {
-      a->vals[r] = vals[m];
-      if (!vals[m]) return fail(SPX_E_ARG, "null vals pointer for operand %d", m);
-    }
+    if (vals) a->vals[r] = vals[m];
   }
   for (int l = 0; l < fam->sparse_levels; ++l) {
     if (pos) a->pos[l] = pos[l];
@@ -85,6 +82,16 @@ int resolve(const spx_plan* plan, const void* const* vals, const int32_t* const*
   for (int l = 0; l < 4; ++l) a->level_sizes[l] = plan->level_sizes[l];
   const int64_t nnz = a->level_sizes[fam->sparse_levels == 1 ? 1 : 2];
   if (nnz < 0 || nnz > INT32_MAX) return fail(SPX_E_ARG, "nnz %lld outside int32 positions", (long long)nnz);
+  if (vals) {
+    // a null buffer is only acceptable for an operand with no elements
+    for (int r = 0; r < fam->nroles; ++r) {
+      int64_t n = 1;
+      if (r == 0) n = nnz;
+      else
+        for (int d = 0; d < fam->order[r]; ++d) n *= a->dims[r][d];
+      if (!a->vals[r] && n > 0) return fail(SPX_E_ARG, "null vals pointer for operand role %d", r);
+    }
+  }
   return SPX_OK;
 }
 
@@ -152,8 +159,10 @@ int spx_launch(const spx_plan* plan, void* out, const void* const* vals, const i
   Args a;
   if (int e = resolve(plan, vals, pos, crd, dims, &fam, &a)) return e;
   if (!vals || !pos || !crd) return fail(SPX_E_ARG, "null argument table");
-  for (int l = 0; l < fam.sparse_levels; ++l)
-    if (!a.pos[l] || !a.crd[l]) return fail(SPX_E_ARG, "null pos/crd for level %d", l);
+  for (int l = 0; l < fam.sparse_levels; ++l) {
+    const int64_t lsize = a.level_sizes[fam.sparse_levels == 1 ? 1 : l];
+    if (!a.pos[l] || (!a.crd[l] && lsize > 0)) return fail(SPX_E_ARG, "null pos/crd for level %d", l);
+  }
   if (!out) return fail(SPX_E_ARG, "null output");
   a.out = out;
   a.ws = workspace;

@@ -458,7 +458,8 @@ int run_spmm(int kid, const Args& a, const SpmmGeom& g) {
     const size_t head_smem = ((size_t)nw * (g.pw * sizeof(T) + sizeof(int32_t)) + 15) & ~size_t(15);
     dim3 grid((unsigned)ncta, (unsigned)g.npanels);
     const uint32_t* hot = nullptr;
-    const int ring = ring_depth();
+    // params[5]: ring depth override (0 = default, <0 = register pipeline)
+    const int ring = a.params[5] != 0 ? (a.params[5] < 0 ? 0 : a.params[5]) : ring_depth();
     if constexpr (CONTIG && (VPL * sizeof(T)) % 16 == 0) {
       if (ring > 0) {
         auto launch = [&](auto kern, int depth) -> int {
