@@ -82,5 +82,28 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     return LIB
 
 
+REF_SRC = Path("/root/reference/pkg")
+REF_DST = ROOT / "baseline" / "_ref"
+
+
+def install_reference() -> None:
+    """Install the unmodified reference front end into baseline/_ref (git-ignored,
+    not gpurun-ignored, so it ships to the GPU box).  Runs only where the
+    read-only source mount exists and the install is missing; the build needs
+    to write into its source tree, so it installs from a copy under /tmp."""
+    if (REF_DST / "spindle" / "schedule.py").exists() or not REF_SRC.is_dir():
+        return
+    import tempfile
+
+    with tempfile.TemporaryDirectory() as tmp:
+        src = Path(tmp) / "pkg"
+        shutil.copytree(REF_SRC, src)
+        cmd = [sys.executable, "-m", "pip", "install", "--no-index", "--no-build-isolation",
+               "--no-deps", "--find-links", "/opt/wheelhouse", "--target", str(REF_DST), str(src)]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            raise RuntimeError(f"reference install failed:\n{res.stdout}\n{res.stderr}")
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))
