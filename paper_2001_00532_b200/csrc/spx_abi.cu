@@ -130,6 +130,28 @@ __global__ void partition_kernel(const int32_t* __restrict__ seg_start, int64_t 
   out[g] = lower_bound(seg_start, 0, nseg, target);
 }
 
+__global__ void chunk_segments_kernel(const int32_t* __restrict__ pos, int64_t nseg, int64_t chunk, int64_t nchunks,
+                                      int32_t* __restrict__ first) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nseg; r += stride) {
+    const int64_t a = __ldcs(pos + r), e = __ldcs(pos + r + 1);
+    // chunks c with a <= c*chunk < e start inside segment r; later segments
+    // start after e and earlier ones end at or before a, so r is the largest
+    // segment with pos[r] <= c*chunk
+    for (int64_t c = (a + chunk - 1) / chunk; c * chunk < e; ++c) first[c] = (int32_t)r;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) first[nchunks] = (int32_t)(nseg > 0 ? nseg - 1 : 0);
+}
+
+int launch_chunk_segments(const int32_t* pos, int64_t nseg, int64_t chunk, int64_t nchunks, int32_t* first,
+                          cudaStream_t stream) {
+  int64_t blocks = ceil_div(nseg > 0 ? nseg : 1, 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  chunk_segments_kernel<<<(unsigned)blocks, 256, 0, stream>>>(pos, nseg, chunk, nchunks, first);
+  count_launch();
+  return check_cuda(cudaGetLastError(), "chunk_segments_kernel");
+}
+
 }  // namespace spx
 
 using namespace spx;

@@ -42,4 +42,28 @@ size_t ws_spmm(int kernel_id, const Args& a);
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Workspace of the nnz-split kernels: per-CTA carry values (`vals_per_cta`
+// elements of `es` bytes), per-CTA carry rows, and the chunk->segment table
+// (ncta + 1 int32).  Offsets are 256 B aligned.
+struct NnzWorkspace {
+  size_t carry_val, carry_row, first, total;
+};
+inline NnzWorkspace nnz_workspace(int64_t ncta, size_t es, int64_t vals_per_cta = 1) {
+  auto up = [](size_t b) { return (b + 255) & ~(size_t)255; };
+  NnzWorkspace w;
+  w.carry_val = 0;
+  w.carry_row = up((size_t)ncta * vals_per_cta * es);
+  w.first = w.carry_row + up((size_t)ncta * sizeof(int32_t));
+  w.total = w.first + up((size_t)(ncta + 1) * sizeof(int32_t));
+  return w;
+}
+
+// first[c] = SearchSegment(pos, 0, nseg, c*chunk) (ir.py:178-190) for every
+// chunk c in [0, nchunks) of `chunk` consecutive leaf positions, computed by
+// one coalesced pass over pos (each nonempty segment writes the chunks whose
+// first position it holds); first[nchunks] = nseg - 1.  Replaces a serial
+// binary search at the start of every CTA/warp of the nnz-split kernels.
+int launch_chunk_segments(const int32_t* pos, int64_t nseg, int64_t chunk, int64_t nchunks, int32_t* first,
+                          cudaStream_t stream);
+
 }  // namespace spx

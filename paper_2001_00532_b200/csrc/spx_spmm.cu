@@ -99,7 +99,8 @@ template <typename T, int VPL, bool CONTIG, int U, int RING>
 __global__ void __launch_bounds__(kMaxThreads) spmm_nnz_kernel(
     const int32_t* __restrict__ pos, const int32_t* __restrict__ crd, const T* __restrict__ vals,
     const T* __restrict__ B, T* __restrict__ C, int64_t M, int64_t N, int64_t nnz, int64_t TB,
-    int64_t W, int32_t* __restrict__ carry_row, T* __restrict__ carry_val, const uint32_t* __restrict__ hot) {
+    int64_t W, int32_t* __restrict__ carry_row, T* __restrict__ carry_val, const uint32_t* __restrict__ hot,
+    const int32_t* __restrict__ first) {
   using F = Frag<T, VPL, CONTIG>;
   constexpr int PW = 32 * VPL;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -121,7 +122,7 @@ __global__ void __launch_bounds__(kMaxThreads) spmm_nnz_kernel(
 
   int32_t head = -1;
   if (q0 < q1) {
-    int64_t r = warp_search_segment(pos, 0, M, q0, lane);  // row holding q0
+    int64_t r = __ldg(first + q0 / W);  // row holding q0 (chunk_segments_kernel)
     const int64_t rstart = __ldg(pos + r);
     bool is_head = rstart < q0;
     if (!is_head && r > 0 && __ldg(pos + r - 1) == q0) {
@@ -245,7 +246,6 @@ __global__ void __launch_bounds__(kMaxThreads) spmm_nnz_kernel(
         nc = ld_i32_first(crd + p + 32 + lane, pol_s);
         nv = ld_stream_hint(vals + p + 32 + lane, pol_s);
       }
-      F buf0[U], buf1[U];
       auto gather = [&](F(&buf)[U], int g) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -273,14 +273,16 @@ __global__ void __launch_bounds__(kMaxThreads) spmm_nnz_kernel(
           if (u0 >= cnt) break;
         }
       };
-      gather(buf0, 0);
-      for (int g = 0; g < G; g += 2) {
+      // Single buffer of U rows in registers: the gathers of one group are
+      // all in flight before the first FMA, and the SM's other warps hide
+      // the latency (occupancy instead of a second buffer: the L1TEX gather
+      // path, ~64 B/clk/SM, is the bound -- profiles/r01_gather_bound.txt)
+#pragma unroll 1
+      for (int g = 0; g < G; ++g) {
         if (g * U >= n) break;
-        if ((g + 1) * U < n) gather(buf1, g + 1);
-        consume(buf0, g);
-        if ((g + 1) * U >= n) break;
-        if (g + 2 < G && (g + 2) * U < n) gather(buf0, g + 2);
-        consume(buf1, g + 1);
+        F buf[U];
+        gather(buf, g);
+        consume(buf, g);
       }
       p += n;
     }
@@ -408,6 +410,15 @@ SpmmGeom spmm_geom(int dtype, int64_t N) {
   return g;
 }
 
+// carry values per (CTA, panel), carry rows per (CTA, panel), and the
+// per-warp-chunk start rows (ncta * warps_per_cta + 1)
+NnzWorkspace spmm_workspace(int64_t ncta, int64_t wpc, const SpmmGeom& g, size_t es) {
+  NnzWorkspace w = nnz_workspace(ncta * g.npanels, es, g.pw);
+  const NnzWorkspace f = nnz_workspace(ncta * wpc, 1, 0);
+  w.total = w.first + (f.total - f.first);
+  return w;
+}
+
 int check_bound(const Args& a, int64_t N) {
   const int ws = a.params[2] ? a.params[2] : 32;
   if (ws != 32)
@@ -450,11 +461,14 @@ int run_spmm(int kid, const Args& a, const SpmmGeom& g) {
     const int nw = (int)(TB / W);
     const int64_t ncta = nnz == 0 ? 1 : ceil_div(nnz, TB);
     if (ncta > INT32_MAX) return fail(SPX_E_ARG, "grid too large");
-    const size_t need = (size_t)ncta * g.npanels * (sizeof(int32_t) + (size_t)g.pw * sizeof(T)) + 256;
-    if (a.ws_bytes < need || !a.ws) return fail(SPX_E_WORKSPACE, "workspace %zu < %zu bytes", a.ws_bytes, need);
-    T* carry_val = static_cast<T*>(a.ws);
-    int32_t* carry_row = reinterpret_cast<int32_t*>(
-        reinterpret_cast<char*>(a.ws) + (((size_t)ncta * g.npanels * g.pw * sizeof(T) + 255) & ~(size_t)255));
+    const NnzWorkspace L = spmm_workspace(ncta, TB / W, g, sizeof(T));
+    if (a.ws_bytes < L.total || !a.ws)
+      return fail(SPX_E_WORKSPACE, "workspace %zu < %zu bytes", a.ws_bytes, L.total);
+    T* carry_val = reinterpret_cast<T*>(static_cast<char*>(a.ws) + L.carry_val);
+    int32_t* carry_row = reinterpret_cast<int32_t*>(static_cast<char*>(a.ws) + L.carry_row);
+    int32_t* first = reinterpret_cast<int32_t*>(static_cast<char*>(a.ws) + L.first);
+    if (nnz > 0)
+      if (int e = launch_chunk_segments(pos, M, W, ncta * (TB / W), first, a.stream)) return e;
     const size_t head_smem = ((size_t)nw * (g.pw * sizeof(T) + sizeof(int32_t)) + 15) & ~size_t(15);
     dim3 grid((unsigned)ncta, (unsigned)g.npanels);
     const uint32_t* hot = nullptr;
@@ -467,7 +481,7 @@ int run_spmm(int kid, const Args& a, const SpmmGeom& g) {
           if (int e = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                                  "cudaFuncSetAttribute"))
             return e;
-          kern<<<grid, nw * 32, smem, a.stream>>>(pos, crd, vals, B, C, M, N, nnz, TB, W, carry_row, carry_val, hot);
+          kern<<<grid, nw * 32, smem, a.stream>>>(pos, crd, vals, B, C, M, N, nnz, TB, W, carry_row, carry_val, hot, first);
           return SPX_OK;
         };
         int e = ring >= 16 ? launch(spmm_nnz_kernel<T, VPL, CONTIG, U, 16>, 16)
@@ -475,11 +489,11 @@ int run_spmm(int kid, const Args& a, const SpmmGeom& g) {
         if (e) return e;
       } else {
         spmm_nnz_kernel<T, VPL, CONTIG, U, 0><<<grid, nw * 32, head_smem, a.stream>>>(
-            pos, crd, vals, B, C, M, N, nnz, TB, W, carry_row, carry_val, hot);
+            pos, crd, vals, B, C, M, N, nnz, TB, W, carry_row, carry_val, hot, first);
       }
     } else {
       spmm_nnz_kernel<T, VPL, CONTIG, U, 0><<<grid, nw * 32, head_smem, a.stream>>>(
-          pos, crd, vals, B, C, M, N, nnz, TB, W, carry_row, carry_val, hot);
+          pos, crd, vals, B, C, M, N, nnz, TB, W, carry_row, carry_val, hot, first);
     }
     count_launch();
     if (int e = check_cuda(cudaGetLastError(), "spmm_nnz_kernel")) return e;
@@ -524,9 +538,10 @@ size_t ws_spmm(int kid, const Args& a) {
   const SpmmGeom g = spmm_geom(a.dtype, N);
   const int64_t nnz = a.level_sizes[1];
   const int64_t TB = a.params[0] > 0 ? a.params[0] : 1;
+  const int64_t W = a.params[1] > 0 ? a.params[1] : TB;
   const int64_t ncta = nnz == 0 ? 1 : ceil_div(nnz, TB);
   const size_t es = a.dtype == SPX_F32 ? 4 : 8;
-  return (size_t)ncta * g.npanels * (sizeof(int32_t) + (size_t)g.pw * es) + 256;
+  return spmm_workspace(ncta, TB / W > 0 ? TB / W : 1, g, es).total;
 }
 
 int launch_spmm(int kid, const Args& a) {

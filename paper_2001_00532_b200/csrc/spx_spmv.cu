@@ -103,136 +103,123 @@ __global__ void __launch_bounds__(kMaxThreads) spmv_nnz_kernel(const int32_t* __
                                                         const T* __restrict__ vals, const T* __restrict__ x,
                                                         T* __restrict__ y, int64_t M, int64_t nnz, int64_t TB,
                                                         int tpt_rt, int32_t* __restrict__ carry_row,
-                                                        T* __restrict__ carry_val) {
+                                                        T* __restrict__ carry_val,
+                                                        const int32_t* __restrict__ first) {
   __shared__ int32_t s_pos[kPosCache];
-  __shared__ int64_t s_rows[2];
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* s_hval = reinterpret_cast<T*>(smem_raw);
   int32_t* s_hrow = reinterpret_cast<int32_t*>(s_hval + blockDim.x);
 
   const int tpt = TPT > 0 ? TPT : tpt_rt;
-  const int tid = threadIdx.x, lane = tid & 31;
+  const int tid = threadIdx.x;
   const int64_t cta = blockIdx.x;
   const int64_t p0 = cta * TB;
   const int64_t p1 = min(p0 + TB, nnz);
   const int64_t a = min(p0 + (int64_t)tid * tpt, p1);
   const int64_t e = min(a + tpt, p1);
+  const int n = (int)(e - a);
 
-  if (p0 < p1) {
-    if (tid < 32) {
-      const int64_t rlo = warp_search_segment(pos, 0, M, p0, lane);
-      const int64_t rhi = warp_search_segment(pos, rlo, M, p1 - 1, lane);
-      if (lane == 0) {
-        s_rows[0] = rlo;
-        s_rows[1] = rhi;
-      }
-    }
-    __syncthreads();
-    const int64_t rlo = s_rows[0], rhi = s_rows[1];
-    const int64_t nstage = rhi - rlo + 2;  // pos[rlo .. rhi+1]
-    const bool staged = nstage <= kPosCache;
-    if (staged)
-      for (int64_t k = tid; k < nstage; k += blockDim.x) s_pos[k] = __ldg(pos + rlo + k);
-    __syncthreads();
-    auto P = [&](int64_t r) -> int64_t {  // pos[r] for r in [rlo, rhi+1]
-      return staged ? (int64_t)s_pos[r - rlo] : (int64_t)__ldg(pos + r);
-    };
-
-    int32_t head = -1;
-    T hval = T(0);
-    if (a < e) {
-      // SearchSegment over the CTA's rows (ir.py:178-190)
-      int64_t lo = rlo, hi = rhi + 1;
-      while (lo < hi) {
-        int64_t mid = (lo + hi) >> 1;
-        if (P(mid) <= a) lo = mid + 1;
-        else hi = mid;
-      }
-      int64_t r = lo - 1;
-      bool is_head = P(r) < a;
-      if (!is_head && r > 0) {
-        // empty rows with pos == a before r are owned by this thread
-        int64_t rr = r - 1;
-        while (rr >= rlo && P(rr) == a) __stcs(y + rr--, T(0));
-        if (rr < rlo && rr >= 0 && __ldg(pos + rr) == a) {
-          int64_t lb = lower_bound(pos, 0, rlo, a);
-          for (int64_t q = lb; q < rlo; ++q) __stcs(y + q, T(0));
-        }
-      }
-      int64_t rend = P(r + 1);
-      T acc = T(0);
-      const int n = (int)(e - a);
-      if constexpr (TPT > 0) {
-        ThreadChunk<T, TPT> ch;
-        ch.load(crd, vals, a, n);
-        T xv[TPT];
-#pragma unroll
-        for (int k = 0; k < TPT; ++k) xv[k] = k < n ? __ldg(x + ch.c[k]) : T(0);
-#pragma unroll
-        for (int k = 0; k < TPT; ++k) {
-          if (k < n) {
-            const int64_t p = a + k;
-            while (p >= rend) {
-              if (is_head) {
-                head = (int32_t)r;
-                hval = acc;
-                is_head = false;
-              } else {
-                __stcs(y + r, acc);
-              }
-              acc = T(0);
-              ++r;
-              rend = P(r + 1);
-            }
-            acc += ch.v[k] * xv[k];
-          }
-        }
-      } else {
-        for (int64_t p = a; p < e; ++p) {
-          const T prod = __ldcs(vals + p) * __ldg(x + __ldcs(crd + p));
-          while (p >= rend) {
-            if (is_head) {
-              head = (int32_t)r;
-              hval = acc;
-              is_head = false;
-            } else {
-              __stcs(y + r, acc);
-            }
-            acc = T(0);
-            ++r;
-            rend = P(r + 1);
-          }
-          acc += prod;
-        }
-      }
-      if (is_head) {
-        head = (int32_t)r;
-        hval = acc;
-      } else {
-        __stcs(y + r, acc);
-      }
-      if (e == nnz)
-        for (int64_t q = r + 1; q < M; ++q) __stcs(y + q, T(0));
-    }
-    s_hrow[tid] = head;
-    s_hval[tid] = hval;
-    __syncthreads();
-    if (head >= 0 && (tid == 0 || s_hrow[tid - 1] != head)) {
-      T s = hval;
-      for (int t2 = tid + 1; t2 < (int)blockDim.x && s_hrow[t2] == head; ++t2) s += s_hval[t2];
-      if (P(head) >= p0) {
-        y[head] = __ldcg(y + head) + s;
-      } else {
-        carry_val[cta] = s;
-        carry_row[cta] = head;
-      }
-    }
-    if (tid == 0 && !(head >= 0 && P(head) < p0)) carry_row[cta] = -1;
-  } else {
+  if (p0 >= p1) {
     if (nnz == 0 && cta == 0)
       for (int64_t q = tid; q < M; q += blockDim.x) __stcs(y + q, T(0));
     if (tid == 0) carry_row[cta] = -1;
+    return;
   }
+  // Issue this thread's (crd, vals) loads and x gathers first so their
+  // latency overlaps the staging of pos below (one dependent global round
+  // trip per phase instead of a serial search chain).
+  ThreadChunk<T, (TPT > 0 ? TPT : 1)> ch;
+  T xv[TPT > 0 ? TPT : 1];
+  if constexpr (TPT > 0) {
+    ch.load(crd, vals, a, n);
+#pragma unroll
+    for (int k = 0; k < TPT; ++k) xv[k] = k < n ? __ldg(x + ch.c[k]) : T(0);
+  }
+  // rows of this chunk: [first[cta], first[cta+1]] (chunk_segments_kernel)
+  const int64_t rlo = __ldg(first + cta), rhi = __ldg(first + cta + 1);
+  const int64_t nstage = rhi - rlo + 2;  // pos[rlo .. rhi+1]
+  const bool staged = nstage <= kPosCache;
+  if (staged)
+    for (int64_t k = tid; k < nstage; k += blockDim.x) s_pos[k] = __ldg(pos + rlo + k);
+  __syncthreads();
+  auto P = [&](int64_t r) -> int64_t {  // pos[r] for r in [rlo, rhi+1]
+    return staged ? (int64_t)s_pos[r - rlo] : (int64_t)__ldg(pos + r);
+  };
+
+  int32_t head = -1;
+  T hval = T(0);
+  if (a < e) {
+    // SearchSegment over the CTA's rows (ir.py:178-190)
+    int64_t lo = rlo, hi = rhi + 1;
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (P(mid) <= a) lo = mid + 1;
+      else hi = mid;
+    }
+    int64_t r = lo - 1;
+    bool is_head = P(r) < a;
+    if (!is_head && r > 0) {
+      // empty rows with pos == a before r are owned by this thread
+      int64_t rr = r - 1;
+      while (rr >= rlo && P(rr) == a) __stcs(y + rr--, T(0));
+      if (rr < rlo && rr >= 0 && __ldg(pos + rr) == a) {
+        int64_t lb = lower_bound(pos, 0, rlo, a);
+        for (int64_t q = lb; q < rlo; ++q) __stcs(y + q, T(0));
+      }
+    }
+    int64_t rend = P(r + 1);
+    T acc = T(0);
+    auto step = [&](int64_t p, T prod) {
+      while (p >= rend) {
+        if (is_head) {
+          head = (int32_t)r;
+          hval = acc;
+          is_head = false;
+        } else {
+          __stcs(y + r, acc);
+        }
+        acc = T(0);
+        ++r;
+        rend = P(r + 1);
+      }
+      acc += prod;
+    };
+    if constexpr (TPT > 0) {
+      if (n == TPT && a + TPT <= rend) {
+        // whole chunk inside one row: plain fold, no tracking
+#pragma unroll
+        for (int k = 0; k < TPT; ++k) acc += ch.v[k] * xv[k];
+      } else {
+#pragma unroll
+        for (int k = 0; k < TPT; ++k)
+          if (k < n) step(a + k, ch.v[k] * xv[k]);
+      }
+    } else {
+      for (int64_t p = a; p < e; ++p) step(p, __ldcs(vals + p) * __ldg(x + __ldcs(crd + p)));
+    }
+    if (is_head) {
+      head = (int32_t)r;
+      hval = acc;
+    } else {
+      __stcs(y + r, acc);
+    }
+    if (e == nnz)
+      for (int64_t q = r + 1; q < M; ++q) __stcs(y + q, T(0));
+  }
+  s_hrow[tid] = head;
+  s_hval[tid] = hval;
+  __syncthreads();
+  if (head >= 0 && (tid == 0 || s_hrow[tid - 1] != head)) {
+    T s = hval;
+    for (int t2 = tid + 1; t2 < (int)blockDim.x && s_hrow[t2] == head; ++t2) s += s_hval[t2];
+    if (P(head) >= p0) {
+      y[head] = __ldcg(y + head) + s;
+    } else {
+      carry_val[cta] = s;
+      carry_row[cta] = head;
+    }
+  }
+  if (tid == 0 && !(head >= 0 && P(head) < p0)) carry_row[cta] = -1;
 }
 
 template <typename T>
@@ -281,20 +268,22 @@ int run_spmv(int kid, const Args& a) {
                 (long long)TB, (long long)W, (long long)TPT);
   const int threads = (int)(TB / TPT);
   const int64_t ncta = nnz == 0 ? 1 : ceil_div(nnz, TB);
-  const size_t need = (size_t)ncta * (sizeof(T) + sizeof(int32_t)) + 256;
-  if (!a.ws || a.ws_bytes < need) return fail(SPX_E_WORKSPACE, "workspace %zu < %zu bytes", a.ws_bytes, need);
-  T* carry_val = static_cast<T*>(a.ws);
-  int32_t* carry_row =
-      reinterpret_cast<int32_t*>(reinterpret_cast<char*>(a.ws) + ((ncta * sizeof(T) + 255) & ~(size_t)255));
+  const NnzWorkspace L = nnz_workspace(ncta, sizeof(T));
+  if (!a.ws || a.ws_bytes < L.total) return fail(SPX_E_WORKSPACE, "workspace %zu < %zu bytes", a.ws_bytes, L.total);
+  T* carry_val = reinterpret_cast<T*>(static_cast<char*>(a.ws) + L.carry_val);
+  int32_t* carry_row = reinterpret_cast<int32_t*>(static_cast<char*>(a.ws) + L.carry_row);
+  int32_t* first = reinterpret_cast<int32_t*>(static_cast<char*>(a.ws) + L.first);
+  if (nnz > 0)
+    if (int e = launch_chunk_segments(pos, M, TB, ncta, first, a.stream)) return e;
   const size_t smem = (size_t)threads * (sizeof(T) + sizeof(int32_t));
   const unsigned g = (unsigned)ncta;
   switch (TPT) {
-    case 4: spmv_nnz_kernel<T, 4><<<g, threads, smem, a.stream>>>(pos, crd, vals, x, y, M, nnz, TB, 4, carry_row, carry_val); break;
-    case 8: spmv_nnz_kernel<T, 8><<<g, threads, smem, a.stream>>>(pos, crd, vals, x, y, M, nnz, TB, 8, carry_row, carry_val); break;
-    case 16: spmv_nnz_kernel<T, 16><<<g, threads, smem, a.stream>>>(pos, crd, vals, x, y, M, nnz, TB, 16, carry_row, carry_val); break;
+    case 4: spmv_nnz_kernel<T, 4><<<g, threads, smem, a.stream>>>(pos, crd, vals, x, y, M, nnz, TB, 4, carry_row, carry_val, first); break;
+    case 8: spmv_nnz_kernel<T, 8><<<g, threads, smem, a.stream>>>(pos, crd, vals, x, y, M, nnz, TB, 8, carry_row, carry_val, first); break;
+    case 16: spmv_nnz_kernel<T, 16><<<g, threads, smem, a.stream>>>(pos, crd, vals, x, y, M, nnz, TB, 16, carry_row, carry_val, first); break;
     default:
       spmv_nnz_kernel<T, 0><<<g, threads, smem, a.stream>>>(pos, crd, vals, x, y, M, nnz, TB, (int)TPT, carry_row,
-                                                            carry_val);
+                                                            carry_val, first);
   }
   count_launch();
   if (int e = check_cuda(cudaGetLastError(), "spmv_nnz_kernel")) return e;
@@ -311,7 +300,7 @@ size_t ws_spmv(int kid, const Args& a) {
   const int64_t TB = a.params[0] > 0 ? a.params[0] : 1;
   const int64_t ncta = nnz == 0 ? 1 : ceil_div(nnz, TB);
   const size_t es = a.dtype == SPX_F32 ? 4 : 8;
-  return (size_t)ncta * (es + sizeof(int32_t)) + 256;
+  return nnz_workspace(ncta, es).total;
 }
 
 int launch_spmv(int kid, const Args& a) {

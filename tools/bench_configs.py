@@ -56,6 +56,11 @@ def time_launch(ex: Executor, flush: torch.Tensor, reps: int, warm: int) -> list
     return ts
 
 
+def pick(schedules, args):
+    only = [x for x in args.only.split(",") if x]
+    return [s for s in schedules if not only or s[0] in only]
+
+
 def rel_err(got: np.ndarray, want: np.ndarray) -> float:
     if want.size == 0:
         return 0.0
@@ -87,7 +92,7 @@ def run_spmv(cfg, A, dtype, schedules, args):
     out = torch.empty(A.M, dtype=Ad.vals.dtype, device=dev)
     want = O.spmv(A.pos, A.crd, vals, x) if not args.no_parity else None
     cb = (4 + es) * A.nnz + 4 * (A.M + 1) + es * A.N + es * A.M
-    for name, params in schedules:
+    for name, params in pick(schedules, args):
         prog = lower(corpus.build(name, **params))
         ex = Executor(prog, {"A": Ad, "x": xd}, out, dtype=dtype)
         ts = time_launch(ex, FLUSH, args.reps, args.warm)
@@ -104,7 +109,7 @@ def run_spmm(cfg, A, schedules, args, ncols=128):
     out = torch.empty(A.M * ncols, dtype=torch.float32, device=dev)
     want = O.spmm(A.pos, A.crd, vals, B) if not args.no_parity else None
     cb = 8 * A.nnz + 4 * (A.M + 1) + 4 * A.N * ncols + 4 * A.M * ncols
-    for name, params in schedules:
+    for name, params in pick(schedules, args):
         prog = lower(corpus.build(name, **params))
         ex = Executor(prog, {"A": Ad, "B": Bd}, out, dtype="f32")
         ts = time_launch(ex, FLUSH, args.reps, args.warm)
@@ -124,7 +129,7 @@ def run_sddmm(cfg, A, schedules, args, K=256):
     out = torch.empty(A.nnz, dtype=torch.float32, device=dev)
     want = O.sddmm(A.pos, A.crd, vals, Cm, Dm) if not args.no_parity else None
     cb = 8 * A.nnz + 4 * (A.M + 1) + 4 * A.M * K + 4 * A.N * K + 4 * A.nnz
-    for name, params in schedules:
+    for name, params in pick(schedules, args):
         prog = lower(corpus.build(name, **params))
         ex = Executor(prog, {"B": Bd, "C": Cd, "D": Dd}, out, dtype="f32", dense_out=False)
         ts = time_launch(ex, FLUSH, args.reps, args.warm)
@@ -149,7 +154,7 @@ def run_csf(cfg, T, schedules, args, R=32):
     info = {"S": S, "F": F, "nnz": nnz}
     want_m = O.mttkrp(T.dims, T.pos, T.crd, vals, Cm, Dm) if not args.no_parity else None
     out = torch.empty(I * R, dtype=torch.float32, device=dev)
-    for name, params in schedules["mttkrp"]:
+    for name, params in pick(schedules["mttkrp"], args):
         prog = lower(corpus.build(name, **params))
         ex = Executor(prog, {"B": Bd, "C": Cd, "D": Dd}, out, dtype="f32")
         ts = time_launch(ex, FLUSH, args.reps, args.warm)
@@ -158,7 +163,7 @@ def run_csf(cfg, T, schedules, args, R=32):
     J = T.dims[1]
     want_t = O.ttv(T.dims, T.pos, T.crd, vals, c) if not args.no_parity else None
     out2 = torch.empty(I * J, dtype=torch.float32, device=dev)
-    for name, params in schedules["ttv"]:
+    for name, params in pick(schedules["ttv"], args):
         prog = lower(corpus.build(name, **params))
         ex = Executor(prog, {"B": Bd, "c": cd}, out2, dtype="f32")
         ts = time_launch(ex, FLUSH, args.reps, args.warm)
@@ -174,6 +179,7 @@ def main():
     ap.add_argument("--reps", type=int, default=16)
     ap.add_argument("--warm", type=int, default=8)
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--only", default="", help="comma list of schedule names to run (default all)")
     args = ap.parse_args()
     PEAK = hbm_peak()
     FLUSH = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
