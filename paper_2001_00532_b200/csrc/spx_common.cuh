@@ -99,6 +99,86 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// base + a*b with one IMAD.WIDE.U32 (32-bit row index times row bytes)
+template <typename P>
+__device__ __forceinline__ const P* addr_wide(const P* base, uint32_t a, uint32_t b) {
+  uint64_t r;
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"(a), "r"(b), "l"(reinterpret_cast<uint64_t>(base)));
+  return reinterpret_cast<const P*>(r);
+}
+
+// cp.async of 4 / 8 bytes (L1-allocating .ca form, the only one these sizes
+// allow) with zero-fill when src_bytes == 0 and an L2 policy.
+__device__ __forceinline__ void cp_async4(uint32_t smem_addr, const void* gptr, int src_bytes, uint64_t pol) {
+  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2, %3;" ::"r"(smem_addr), "l"(gptr),
+               "r"(src_bytes), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async8(uint32_t smem_addr, const void* gptr, int src_bytes, uint64_t pol) {
+  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2, %3;" ::"r"(smem_addr), "l"(gptr),
+               "r"(src_bytes), "l"(pol)
+               : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// Per-warp ring of leaf batches: (crd, val) of 32 consecutive positions per
+// slot, streamed from HBM into shared memory by cp.async RING-1 batches
+// ahead of use, so a single warp keeps ~RING*32*(4+sizeof(T)) bytes of the
+// sparse operand in flight without holding registers for them.  Slot layout:
+// 32 int32 coordinates then 32 values, so four leaves are read back as one
+// 16-byte broadcast of coordinates and one (or two) of values.
+// ---------------------------------------------------------------------------
+template <typename T, int RING>
+struct LeafRing {
+  static constexpr int kSlotBytes = 32 * (4 + (int)sizeof(T));
+  static constexpr int kBytes = RING * kSlotBytes;
+  unsigned char* base;  // this warp's RING slots
+  const int32_t* crd;
+  const T* vals;
+  int q0, q1, nb;
+
+  __device__ __forceinline__ void init(unsigned char* warp_base, const int32_t* c, const T* v, int a, int b) {
+    base = warp_base;
+    crd = c;
+    vals = v;
+    q0 = a;
+    q1 = b;
+    nb = (b - a + 31) >> 5;
+  }
+  __device__ __forceinline__ const int32_t* crd_slot(int b) const {
+    return reinterpret_cast<const int32_t*>(base + (b % RING) * kSlotBytes);
+  }
+  __device__ __forceinline__ const T* val_slot(int b) const {
+    return reinterpret_cast<const T*>(base + (b % RING) * kSlotBytes + 128);
+  }
+  __device__ __forceinline__ void issue(int b, int lane, uint64_t pol) {
+    if (b < nb) {
+      const int p = q0 + b * 32 + lane;
+      const bool ok = p < q1;
+      const int pp = ok ? p : q0;
+      const uint32_t s = (uint32_t)__cvta_generic_to_shared(base + (b % RING) * kSlotBytes);
+      cp_async4(s + lane * 4, crd + pp, ok ? 4 : 0, pol);
+      if constexpr (sizeof(T) == 8)
+        cp_async8(s + 128 + lane * 8, vals + pp, ok ? 8 : 0, pol);
+      else
+        cp_async4(s + 128 + lane * 4, vals + pp, ok ? 4 : 0, pol);
+    }
+    cp_async_commit();
+  }
+  __device__ __forceinline__ void prologue(int lane, uint64_t pol) {
+#pragma unroll
+    for (int b = 0; b < RING - 1; ++b) issue(b, lane, pol);
+  }
+  // make batch b readable by the whole warp (issues batch b+RING-1)
+  __device__ __forceinline__ void acquire(int b, int lane, uint64_t pol) {
+    issue(b + RING - 1, lane, pol);
+    cp_async_wait<RING - 1>();
+    __syncwarp();
+  }
+  // all lanes are done reading batch b's slot
+  __device__ __forceinline__ void release() { __syncwarp(); }
+};
+
 // ---------------------------------------------------------------------------
 // Per-lane row fragments: a lane owns VPL values of a dense row.
 // CONTIG: lane owns columns [lane*VPL, lane*VPL+VPL) -> vector loads.
@@ -140,6 +220,28 @@ struct Frag {
         int k = i * 32 + lane;
         v[i] = k < ncols ? __ldg(row + k) : T(0);
       }
+    }
+  }
+
+  // CONTIG: load this lane's VPL contiguous values starting at p (p already
+  // includes the lane offset), vectorised
+  __device__ __forceinline__ void load_ptr(const T* __restrict__ p) {
+    constexpr int BYTES = VPL * (int)sizeof(T);
+    if constexpr (BYTES % 16 == 0) {
+#pragma unroll
+      for (int c = 0; c < BYTES / 16; ++c) {
+        float4 q = __ldg(reinterpret_cast<const float4*>(p) + c);
+        *reinterpret_cast<float4*>(&v[c * (16 / sizeof(T))]) = q;
+      }
+    } else if constexpr (BYTES % 8 == 0) {
+#pragma unroll
+      for (int c = 0; c < BYTES / 8; ++c) {
+        float2 q = __ldg(reinterpret_cast<const float2*>(p) + c);
+        *reinterpret_cast<float2*>(&v[c * (8 / sizeof(T))]) = q;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) v[i] = __ldg(p + i);
     }
   }
 

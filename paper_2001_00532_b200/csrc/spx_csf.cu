@@ -26,6 +26,15 @@
 namespace spx {
 namespace {
 
+// K7 TTV: persistent CTAs stage c in shared memory (when it fits) and their
+// warps take fiber groups of FIBERS_PER_WARP fibers round-robin.  A group's
+// leaves are one contiguous position range; the warp streams it 32 leaves
+// at a time (one per lane), forms v*c[k] and folds fibers with a segmented
+// shuffle scan whose head flags come from the fibers' start positions.  The
+// lane that ends a fiber stores A[i,j] (each (i,j) is one fiber, so plain
+// stores); a fiber that continues past the batch is carried in a register.
+constexpr int kTtvRing = 8;
+
 template <typename T>
 __global__ void __launch_bounds__(kMaxThreads) ttv_fiber_kernel(const int32_t* __restrict__ crd0,
                                                          const int32_t* __restrict__ pos1,
@@ -34,141 +43,257 @@ __global__ void __launch_bounds__(kMaxThreads) ttv_fiber_kernel(const int32_t* _
                                                          const int32_t* __restrict__ crd2,
                                                          const T* __restrict__ vals, const T* __restrict__ c,
                                                          T* __restrict__ A, int64_t S, int64_t F, int64_t J,
-                                                         int64_t FTB, int64_t FW) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t f0 = min((int64_t)blockIdx.x * FTB + (int64_t)warp * FW, F);
-  const int64_t f1 = min(min(f0 + FW, (int64_t)(blockIdx.x + 1) * FTB), F);
-  if (f0 >= f1) return;
-  int64_t s = warp_search_segment(pos1, 0, S, f0, lane);
-  int64_t send = __ldg(pos1 + s + 1);
-  for (int64_t f = f0; f < f1; ++f) {
-    while (f >= send) {
-      ++s;
-      send = __ldg(pos1 + s + 1);
-    }
-    const int64_t a = __ldg(pos2 + f), e = __ldg(pos2 + f + 1);
-    T acc = T(0);
-    for (int64_t p = a + lane; p < e; p += 32) acc += __ldcs(vals + p) * __ldg(c + __ldcs(crd2 + p));
+                                                         int64_t K, int64_t FW, int64_t ngroups, int c_in_smem) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  if (c_in_smem) {
+    T* sc0 = reinterpret_cast<T*>(smem_raw + (size_t)(blockDim.x >> 5) * LeafRing<T, kTtvRing>::kBytes);
+    for (int64_t k = threadIdx.x; k < K; k += blockDim.x) sc0[k] = __ldg(c + k);
+    __syncthreads();
+  }
+  const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* ring_base = smem_raw + (size_t)warp * LeafRing<T, kTtvRing>::kBytes;
+  T* sc = reinterpret_cast<T*>(smem_raw + (size_t)nw * LeafRing<T, kTtvRing>::kBytes);
+  const uint64_t pol_s = l2_evict_first();
+  for (int64_t g = (int64_t)blockIdx.x * nw + warp; g < ngroups; g += (int64_t)gridDim.x * nw) {
+    const int gf1 = (int)min(g * FW + FW, F);
+    int sl = -1;
+    // sub-groups of 32 fibers: one lane per fiber holds its start position
+    // and its output offset A[i*J + j]
+    for (int f0 = (int)(g * FW); f0 < gf1; f0 += 32) {
+      const int f1 = min(f0 + 32, gf1);
+      const int myfib = f0 + lane;
+      const int st_mine = __ldg(pos2 + min(myfib, f1));
+      if (sl < 0) sl = (int)warp_search_segment(pos1, 0, S, f0, lane);
+      int s_mine = sl;
+      if (myfib < f1)
+        while (__ldg(pos1 + s_mine + 1) <= myfib) ++s_mine;
+      const int64_t off_mine = myfib < f1 ? (int64_t)__ldg(crd0 + s_mine) * J + __ldg(crd1 + myfib) : 0;
+      sl = __shfl_sync(kFull, s_mine, f1 - f0 - 1);
+      const int q0 = __shfl_sync(kFull, st_mine, 0), q1 = __ldg(pos2 + f1);
+      const bool is_start = myfib < f1;
+      int fcur = 0;  // fiber (relative to f0) holding position p
+      T carry = T(0);
+      LeafRing<T, kTtvRing> ring;
+      ring.init(ring_base, crd2, vals, q0, q1);
+      ring.prologue(lane, pol_s);
+      for (int b = 0; b < ring.nb; ++b) {
+        ring.acquire(b, lane, pol_s);
+        const int p = q0 + b * 32;
+        const int n = min(32, q1 - p);
+        const int kk = ring.crd_slot(b)[lane];
+        const T vv = ring.val_slot(b)[lane];
+        ring.release();
+        T x = T(0);
+        if (lane < n) x = vv * (c_in_smem ? sc[kk] : __ldg(c + kk));
+        // head flags: bit t set when position p+t starts a fiber
+        const unsigned H =
+            __reduce_or_sync(kFull, (is_start && st_mine >= p && st_mine < p + n) ? (1u << (st_mine - p)) : 0u);
+        const unsigned upto = H & (lane == 31 ? kFull : ((2u << lane) - 1u));
+        const int sstart = upto ? 31 - __clz(upto) : 0;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
-    if (lane == 0) A[(int64_t)__ldg(crd0 + s) * J + __ldg(crd1 + f)] = acc;
+        for (int o = 1; o < 32; o <<= 1) {
+          const T y = __shfl_up_sync(kFull, x, o);
+          if (lane - o >= sstart) x += y;
+        }
+        if (!upto) x += carry;  // continues the fiber open at the previous batch
+        const int myf = fcur + __popc(upto) - (int)(H & 1u);
+        const int lastf = fcur + __popc(H) - (int)(H & 1u);
+        const int nxt = __shfl_sync(kFull, st_mine, (lastf + 1) & 31);  // start of the next fiber
+        const int lastend = lastf + 1 >= f1 - f0 ? q1 : nxt;
+        const bool ends_here = lane < n && ((lane + 1 < n && ((H >> (lane + 1)) & 1u)) ||
+                                            (lane == n - 1 && lastend == p + n));
+        const int64_t off = __shfl_sync(kFull, off_mine, myf & 31);
+        if (ends_here) A[off] = x;
+        const T tail = __shfl_sync(kFull, x, n - 1);
+        if (lastend == p + n) {
+          carry = T(0);
+          fcur = lastf + 1;
+        } else {
+          carry = tail;
+          fcur = lastf;
+        }
+      }
+    }
   }
 }
 
-template <typename T, int VPL, bool CONTIG, int U>
-__global__ void __launch_bounds__(kMaxThreads) mttkrp_nnz_kernel(
-    const int32_t* __restrict__ crd0, const int32_t* __restrict__ pos1, const int32_t* __restrict__ crd1,
-    const int32_t* __restrict__ pos2, const int32_t* __restrict__ crd2, const T* __restrict__ vals,
-    const T* __restrict__ Cm, const T* __restrict__ Dm, T* __restrict__ A, int64_t S, int64_t F, int64_t nnz,
-    int64_t R, int64_t TB, int64_t W) {
+// ---------------------------------------------------------------------------
+// MTTKRP leaf-range engine shared by K8 (nnz-split) and K9 (slice-split).
+//
+// A warp walks a contiguous range of leaf positions [q0, q1) of B (level 2)
+// with its lanes over the rank dimension j.  The (l, v) of the leaves stream
+// through a per-warp cp.async ring (LeafRing) and are read back four at a
+// time as 16-byte broadcasts; per leaf the warp then issues one row read of
+// D (L1-resident: 256 KB at cfg4) and VPL FFMAs, so the D row read (128 B at
+// R=32 fp32) is the per-leaf cost.  The fiber partial sum_l B*D[l,:] is
+// scaled by C[k,:] when the fiber ends (the C row is prefetched when the
+// fiber starts) and the slice partial goes to A[i,:] when the slice ends:
+// red.global.add for chunks that may share a slice (the schedule's Atomics
+// strategy), a plain store for a warp that owns the whole slice.
+// ---------------------------------------------------------------------------
+constexpr int kLeafRing = 4;
+
+template <typename T, int VPL, bool CONTIG>
+struct MttkrpCtx {
+  const int32_t *crd0, *pos1, *crd1, *pos2, *crd2;
+  const T *vals, *Cm, *Dm;
+  T* A;
+  int64_t S, F, R;
+};
+
+// Walk leaves [q0, q1); f = fiber holding q0, s = slice holding f.
+// OWNED: the warp owns every slice it touches completely (plain stores).
+template <typename T, int VPL, bool CONTIG, bool OWNED>
+__device__ __forceinline__ void mttkrp_walk(const MttkrpCtx<T, VPL, CONTIG>& c, unsigned char* ring_base, int lane,
+                                            int q0, int q1, int f, int s) {
   using Fr = Frag<T, VPL, CONTIG>;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t p0 = (int64_t)blockIdx.x * TB;
-  const int64_t p1 = min(p0 + TB, nnz);
-  const int64_t q0 = min(p0 + (int64_t)warp * W, p1);
-  const int64_t q1 = min(q0 + W, p1);
-  if (q0 >= q1) return;
-  const int ncols = (int)R;
-  int64_t f = warp_search_segment(pos2, 0, F, q0, lane);
-  int64_t s = warp_search_segment(pos1, 0, S, f, lane);
-  RowEndCache fends;
-  fends.fill(pos2, f, F, lane);
-  int64_t fend = fends.end(pos2, f, F, lane);
-  int64_t send = __ldg(pos1 + s + 1);
+  const int ncols = (int)c.R;
+  const int Ri = (int)c.R;
+  const uint64_t pol_s = l2_evict_first();
+  // fibers [fb, fb+32): ends and k coordinates, one per lane
+  int fb = f;
+  int fe_mine = __ldg(c.pos2 + min((int64_t)fb + 1 + lane, c.F));
+  int k_mine = __ldg(c.crd1 + min((int64_t)fb + lane, c.F - 1));
+  auto fiber_end = [&](int ff) -> int {
+    if (ff - fb >= 32) {
+      fb = ff;
+      fe_mine = __ldg(c.pos2 + min((int64_t)fb + 1 + lane, c.F));
+      k_mine = __ldg(c.crd1 + min((int64_t)fb + lane, c.F - 1));
+    }
+    return __shfl_sync(kFull, fe_mine, ff - fb);
+  };
+  auto fiber_k = [&](int ff) -> int { return __shfl_sync(kFull, k_mine, ff - fb); };
+  int fend = fiber_end(f);
+  int send = __ldg(c.pos1 + s + 1);
   Fr accf, accs, crow;
   accf.zero();
   accs.zero();
-  for (int64_t p = q0; p < q1; p += 32) {
-    const int n = (int)min((int64_t)32, q1 - p);
-    int my_l = 0;
-    T my_v = T(0);
-    if (lane < n) {
-      my_l = __ldcs(crd2 + p + lane);
-      my_v = __ldcs(vals + p + lane);
-    }
-    for (int t0 = 0; t0 < n; t0 += U) {
-      Fr d[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int l = __shfl_sync(kFull, my_l, (t0 + u) & 31);
-        if (t0 + u < n) d[u].load(Dm + (int64_t)l * R, lane, ncols);
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (t0 + u < n) {
-          const T v = __shfl_sync(kFull, my_v, (t0 + u) & 31);
-          const int64_t pp = p + t0 + u;
-          while (pp >= fend) {
-            crow.load(Cm + (int64_t)__ldg(crd1 + f) * R, lane, ncols);
-#pragma unroll
-            for (int i = 0; i < VPL; ++i) accs.v[i] += accf.v[i] * crow.v[i];
-            accf.zero();
-            ++f;
-            fend = fends.end(pos2, f, F, lane);
-            while (f >= send) {
-              accs.atomic_add_into(A + (int64_t)__ldg(crd0 + s) * R, lane, ncols);
-              accs.zero();
-              ++s;
-              send = __ldg(pos1 + s + 1);
-            }
-          }
-          accf.fma(v, d[u]);
-        }
-      }
-    }
-  }
-  crow.load(Cm + (int64_t)__ldg(crd1 + f) * R, lane, ncols);
-#pragma unroll
-  for (int i = 0; i < VPL; ++i) accs.v[i] += accf.v[i] * crow.v[i];
-  accs.atomic_add_into(A + (int64_t)__ldg(crd0 + s) * R, lane, ncols);
-}
-
-template <typename T, int VPL, bool CONTIG, int U>
-__global__ void __launch_bounds__(kMaxThreads) mttkrp_slice_kernel(
-    const int32_t* __restrict__ crd0, const int32_t* __restrict__ pos1, const int32_t* __restrict__ crd1,
-    const int32_t* __restrict__ pos2, const int32_t* __restrict__ crd2, const T* __restrict__ vals,
-    const T* __restrict__ Cm, const T* __restrict__ Dm, T* __restrict__ A, int64_t S, int64_t R, int64_t CH) {
-  using Fr = Frag<T, VPL, CONTIG>;
-  const int nw = blockDim.x >> 5;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ncols = (int)R;
-  const int64_t lo = (int64_t)blockIdx.x * CH;
-  for (int64_t k = warp; k < CH; k += nw) {
-    const int64_t s = lo + k;
-    if (s >= S) return;
-    Fr accs, accf, crow;
+  crow.load(c.Cm + fiber_k(f) * Ri, lane, ncols);
+  auto flush_slice = [&]() {
+    T* dst = c.A + (int64_t)__ldg(c.crd0 + s) * c.R;
+    if constexpr (OWNED) accs.store(dst, lane, ncols);
+    else accs.atomic_add_into(dst, lane, ncols);
     accs.zero();
-    for (int64_t f = __ldg(pos1 + s); f < __ldg(pos1 + s + 1); ++f) {
-      accf.zero();
-      const int64_t a = __ldg(pos2 + f), e = __ldg(pos2 + f + 1);
-      for (int64_t p = a; p < e; p += 32) {
-        const int n = (int)min((int64_t)32, e - p);
-        int my_l = 0;
-        T my_v = T(0);
-        if (lane < n) {
-          my_l = __ldcs(crd2 + p + lane);
-          my_v = __ldcs(vals + p + lane);
-        }
-        for (int t0 = 0; t0 < n; t0 += U) {
-          Fr d[U];
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const int l = __shfl_sync(kFull, my_l, (t0 + u) & 31);
-            if (t0 + u < n) d[u].load(Dm + (int64_t)l * R, lane, ncols);
-          }
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const T v = __shfl_sync(kFull, my_v, (t0 + u) & 31);
-            if (t0 + u < n) accf.fma(v, d[u]);
-          }
-        }
-      }
-      crow.load(Cm + (int64_t)__ldg(crd1 + f) * R, lane, ncols);
+  };
+  // close fibers until position pp lies inside fiber f
+  auto advance_to = [&](int pp) {
+    while (pp >= fend) {
 #pragma unroll
       for (int i = 0; i < VPL; ++i) accs.v[i] += accf.v[i] * crow.v[i];
+      accf.zero();
+      ++f;
+      fend = fiber_end(f);
+      while (f >= send) {
+        flush_slice();
+        ++s;
+        send = __ldg(c.pos1 + s + 1);
+      }
+      crow.load(c.Cm + fiber_k(f) * Ri, lane, ncols);
     }
-    accs.store(A + (int64_t)__ldg(crd0 + s) * R, lane, ncols);
+  };
+  // this lane's slice of D: row l starts at Dl + l*R (32-bit offsets)
+  const char* __restrict__ Dl = reinterpret_cast<const char*>(c.Dm + (CONTIG ? lane * VPL : lane));
+  const uint32_t rowb = (uint32_t)(c.R * (int64_t)sizeof(T));
+  auto drow = [&](Fr& d, int l) {
+    const T* src = reinterpret_cast<const T*>(addr_wide(Dl, (uint32_t)l, rowb));
+    if constexpr (CONTIG) {
+      d.load_ptr(src);
+    } else {
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) d.v[i] = (i * 32 + lane < ncols) ? __ldg(src + i * 32) : T(0);
+    }
+  };
+  LeafRing<T, kLeafRing> ring;
+  ring.init(ring_base, c.crd2, c.vals, q0, q1);
+  ring.prologue(lane, pol_s);
+  for (int b = 0; b < ring.nb; ++b) {
+    ring.acquire(b, lane, pol_s);
+    const int p = q0 + b * 32;
+    const int n = min(32, q1 - p);
+    const int32_t* Ls = ring.crd_slot(b);
+    const T* Vs = ring.val_slot(b);
+    // aligned groups of four leaves: one 16 B broadcast of coordinates, four
+    // row reads of D; a group that crosses a fiber end takes the slow path
+#pragma unroll 2
+    for (int t = 0; t < n; t += 4) {
+      const int4 l4 = *reinterpret_cast<const int4*>(Ls + t);  // zero-filled past n
+      Fr d0, d1, d2, d3;
+      drow(d0, l4.x);
+      drow(d1, l4.y);
+      drow(d2, l4.z);
+      drow(d3, l4.w);
+      if (p + t + 4 <= fend && t + 4 <= n) {
+        accf.fma(Vs[t], d0);
+        accf.fma(Vs[t + 1], d1);
+        accf.fma(Vs[t + 2], d2);
+        accf.fma(Vs[t + 3], d3);
+      } else {
+        const Fr* dd[4] = {&d0, &d1, &d2, &d3};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (t + u < n) {
+            if (p + t + u >= fend) advance_to(p + t + u);
+            accf.fma(Vs[t + u], *dd[u]);
+          }
+        }
+      }
+    }
+    ring.release();
   }
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) accs.v[i] += accf.v[i] * crow.v[i];
+  flush_slice();
+}
+
+constexpr int kMttkrpThreads = 512;
+constexpr size_t kSmemBudget = 200 * 1024;
+
+// K8: persistent CTAs; warp-chunk q covers leaves [q*W, (q+1)*W) (the
+// schedule's `warp` variable; NNZ_PER_TB/NNZ_PER_WARP chunks make a `block`).
+template <typename T, int VPL, bool CONTIG>
+__global__ void __launch_bounds__(kMttkrpThreads, 2) mttkrp_nnz_kernel(
+    const int32_t* __restrict__ crd0, const int32_t* __restrict__ pos1, const int32_t* __restrict__ crd1,
+    const int32_t* __restrict__ pos2, const int32_t* __restrict__ crd2, const T* __restrict__ vals,
+    const T* __restrict__ Cm, const T* __restrict__ Dm, T* __restrict__ A, int64_t S, int64_t F, int64_t nnz,
+    int64_t R, int64_t W, int64_t nchunks, const int32_t* __restrict__ first) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* ring = smem_raw + (size_t)warp * LeafRing<T, kLeafRing>::kBytes;
+  MttkrpCtx<T, VPL, CONTIG> c{crd0, pos1, crd1, pos2, crd2, vals, Cm, Dm, A, S, F, R};
+  for (int64_t q = (int64_t)blockIdx.x * nw + warp; q < nchunks; q += (int64_t)gridDim.x * nw) {
+    const int q0 = (int)(q * W);
+    const int q1 = (int)min(q * W + W, nnz);
+    const int f = __ldg(first + q);
+    const int s = (int)warp_search_segment(pos1, 0, S, f, lane);
+    mttkrp_walk<T, VPL, CONTIG, false>(c, ring, lane, q0, q1, f, s);
+  }
+}
+
+// K9: slice-split (A.5 shape) -- one warp per slice, plain stores;
+// persistent CTAs walk the slices round-robin.
+template <typename T, int VPL, bool CONTIG>
+__global__ void __launch_bounds__(kMttkrpThreads, 2) mttkrp_slice_kernel(
+    const int32_t* __restrict__ crd0, const int32_t* __restrict__ pos1, const int32_t* __restrict__ crd1,
+    const int32_t* __restrict__ pos2, const int32_t* __restrict__ crd2, const T* __restrict__ vals,
+    const T* __restrict__ Cm, const T* __restrict__ Dm, T* __restrict__ A, int64_t S, int64_t F, int64_t R) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* ring = smem_raw + (size_t)warp * LeafRing<T, kLeafRing>::kBytes;
+  MttkrpCtx<T, VPL, CONTIG> c{crd0, pos1, crd1, pos2, crd2, vals, Cm, Dm, A, S, F, R};
+  for (int64_t s = (int64_t)blockIdx.x * nw + warp; s < S; s += (int64_t)gridDim.x * nw) {
+    const int f0 = __ldg(pos1 + s), f1 = __ldg(pos1 + s + 1);
+    const int q0 = __ldg(pos2 + f0), q1 = __ldg(pos2 + f1);
+    if (q0 < q1) mttkrp_walk<T, VPL, CONTIG, true>(c, ring, lane, q0, q1, f0, (int)s);
+  }
+}
+
+int num_sms() {
+  static int n = [] {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v > 0 ? v : 148;
+  }();
+  return n;
 }
 
 struct Csf {
@@ -192,7 +317,7 @@ Csf csf_of(const Args& a) {
 template <typename T>
 int run_ttv(const Args& a) {
   const Csf c = csf_of(a);
-  const int64_t I = a.dims[0][0], J = a.dims[0][1];
+  const int64_t I = a.dims[0][0], J = a.dims[0][1], K = a.dims[0][2];
   T* A = static_cast<T*>(a.out);
   if (int e = check_cuda(cudaMemsetAsync(A, 0, (size_t)(I * J) * sizeof(T), a.stream), "memset")) return e;
   if (c.F == 0) return SPX_OK;
@@ -200,17 +325,29 @@ int run_ttv(const Args& a) {
   const int64_t FW = a.params[1] > 0 ? a.params[1] : 32;
   const int64_t nw = ceil_div(FTB, FW);
   if (nw > kMaxWarps) return fail(SPX_E_UNSUPPORTED, "TTV: FIBERS_PER_TB/FIBERS_PER_WARP must be <= 16");
-  ttv_fiber_kernel<T><<<(unsigned)ceil_div(c.F, FTB), (unsigned)(nw * 32), 0, a.stream>>>(
-      c.crd0, c.pos1, c.crd1, c.pos2, c.crd2, static_cast<const T*>(a.vals[0]), static_cast<const T*>(a.vals[1]), A,
-      c.S, c.F, J, FTB, FW);
+  const size_t cbytes = (size_t)K * sizeof(T);
+  const size_t rbytes = (size_t)nw * LeafRing<T, kTtvRing>::kBytes;
+  const int c_in_smem = cbytes + rbytes <= kSmemBudget ? 1 : 0;
+  const size_t smem = rbytes + (c_in_smem ? cbytes : 0);
+  auto kern = ttv_fiber_kernel<T>;
+  if (int e = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                         "cudaFuncSetAttribute"))
+    return e;
+  // persistent: as many CTAs as fit (smem-limited when c is large)
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (int)(nw * 32), smem);
+  if (per_sm < 1) per_sm = 1;
+  const int64_t grid = min((int64_t)num_sms() * per_sm, ceil_div(ceil_div(c.F, FW), nw));
+  kern<<<(unsigned)grid, (unsigned)(nw * 32), smem, a.stream>>>(c.crd0, c.pos1, c.crd1, c.pos2, c.crd2,
+                                                                 static_cast<const T*>(a.vals[0]),
+                                                                 static_cast<const T*>(a.vals[1]), A, c.S, c.F, J, K,
+                                                                 FW, ceil_div(c.F, FW), c_in_smem);
   count_launch();
   return check_cuda(cudaGetLastError(), "ttv_fiber_kernel");
 }
 
 template <typename T, int VPL, bool CONTIG>
 int run_mttkrp(int kid, const Args& a) {
-  constexpr int words = VPL * (int)sizeof(T) / 4;
-  constexpr int U = words >= 8 ? 4 : 8;
   const Csf c = csf_of(a);
   const int64_t I = a.dims[0][0], R = a.dims[1][1];
   T* A = static_cast<T*>(a.out);
@@ -219,20 +356,32 @@ int run_mttkrp(int kid, const Args& a) {
   const T* Dm = static_cast<const T*>(a.vals[2]);
   if (int e = check_cuda(cudaMemsetAsync(A, 0, (size_t)(I * R) * sizeof(T), a.stream), "memset")) return e;
   if (c.nnz == 0) return SPX_OK;
+  const int nw = kMttkrpThreads / 32;
+  const size_t smem = (size_t)nw * LeafRing<T, kLeafRing>::kBytes;
+  auto grid_for = [&](auto kern, int64_t units) -> int64_t {
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kMttkrpThreads, smem);
+    if (per_sm < 1) per_sm = 1;
+    return min((int64_t)num_sms() * per_sm, ceil_div(units, nw));
+  };
   if (kid == SPX_K_MTTKRP_NNZ) {
     const int64_t TB = a.params[0], W = a.params[1];
     if (TB < 1 || W < 1 || TB % W != 0 || TB / W > kMaxWarps)
       return fail(SPX_E_UNSUPPORTED, "MTTKRP nnz-split needs NNZ_PER_TB a multiple of NNZ_PER_WARP, <= 16 warps");
-    mttkrp_nnz_kernel<T, VPL, CONTIG, U><<<(unsigned)ceil_div(c.nnz, TB), (unsigned)(TB / W * 32), 0, a.stream>>>(
-        c.crd0, c.pos1, c.crd1, c.pos2, c.crd2, vals, Cm, Dm, A, c.S, c.F, c.nnz, R, TB, W);
+    const int64_t nchunks = ceil_div(c.nnz, W);
+    if (!a.ws || a.ws_bytes < (size_t)(nchunks + 1) * sizeof(int32_t))
+      return fail(SPX_E_WORKSPACE, "workspace %zu < %zu bytes", a.ws_bytes, (size_t)(nchunks + 1) * 4);
+    int32_t* first = static_cast<int32_t*>(a.ws);
+    if (int e = launch_chunk_segments(c.pos2, c.F, W, nchunks, first, a.stream)) return e;
+    auto kern = mttkrp_nnz_kernel<T, VPL, CONTIG>;
+    kern<<<(unsigned)grid_for(kern, nchunks), kMttkrpThreads, smem, a.stream>>>(
+        c.crd0, c.pos1, c.crd1, c.pos2, c.crd2, vals, Cm, Dm, A, c.S, c.F, c.nnz, R, W, nchunks, first);
     count_launch();
     return check_cuda(cudaGetLastError(), "mttkrp_nnz_kernel");
   }
-  const int64_t CH = a.params[0] > 0 ? a.params[0] : 8;
-  int64_t nw = a.params[1] > 0 ? a.params[1] : (CH < 8 ? CH : 8);
-  if (nw > kMaxWarps) nw = kMaxWarps;
-  mttkrp_slice_kernel<T, VPL, CONTIG, U><<<(unsigned)ceil_div(c.S, CH), (unsigned)(nw * 32), 0, a.stream>>>(
-      c.crd0, c.pos1, c.crd1, c.pos2, c.crd2, vals, Cm, Dm, A, c.S, R, CH);
+  auto kern = mttkrp_slice_kernel<T, VPL, CONTIG>;
+  kern<<<(unsigned)grid_for(kern, c.S), kMttkrpThreads, smem, a.stream>>>(c.crd0, c.pos1, c.crd1, c.pos2, c.crd2,
+                                                                         vals, Cm, Dm, A, c.S, c.F, R);
   count_launch();
   return check_cuda(cudaGetLastError(), "mttkrp_slice_kernel");
 }
@@ -260,6 +409,13 @@ int dispatch_mttkrp(int kid, const Args& a, int64_t R) {
 }
 
 }  // namespace
+
+size_t ws_csf(int kid, const Args& a) {
+  if (kid != SPX_K_MTTKRP_NNZ) return 0;
+  const int64_t nnz = a.level_sizes[2];
+  const int64_t W = a.params[1] > 0 ? a.params[1] : 1;
+  return (size_t)(ceil_div(nnz, W) + 1) * sizeof(int32_t);
+}
 
 int launch_csf(int kid, const Args& a) {
   if (kid == SPX_K_TTV_FIBER) {
