@@ -73,7 +73,7 @@ extern "C" {
  *  2   SpMV warp-per-row         "                        [0]=ROWS_PER_TB [1]=WARPS_PER_TB
  *  3   SpMV nnz-split            "                        [0]=NNZ_PER_TB [1]=NNZ_PER_WARP [2]=NNZ_PER_THREAD
  *  4   SpMM nnz-split            C(i,k)=A(i,j)*B(j,k)     [0]=NNZ_PER_TB [1]=NNZ_PER_WARP [2]=WARP_SIZE [3]=bound (0 = none)
- *                                                         [5]=row-ring depth (0 = default 8, <0 = register pipeline)
+ *                                                         [5]=B-row transport: 0 = default (staged-register path), >0 = cp.async row ring of that depth, <0 = staged-register path
  *  5   SpMM warp-per-row         "                        [0]=ROWS_PER_TB [1]=WARPS_PER_TB [2]=WARP_SIZE [3]=bound
  *  6   SDDMM nnz-split           A(i,j)=B(i,j)*C(i,k)*D(j,k)  [0]=NNZ_PER_TB [1]=NNZ_PER_WARP [2]=WARP_SIZE [3]=bound [7]=dense_out
  *  7   TTV fiber-split           A(i,j)=B(i,j,k)*c(k) B:sss   [0]=FIBERS_PER_TB [1]=FIBERS_PER_WARP

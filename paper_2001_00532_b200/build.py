@@ -31,6 +31,7 @@ NVCC_FLAGS = [
     "-Xptxas",
     "-v" if os.environ.get("SPX_PTXAS_VERBOSE") else "-O3",
     "-I" + str(ROOT / "include"),
+    *os.environ.get("SPX_NVCC_EXTRA", "").split(),
 ]
 
 

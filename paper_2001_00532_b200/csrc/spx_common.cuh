@@ -245,6 +245,20 @@ struct Frag {
     }
   }
 
+  // load_ptr with an L2 eviction-priority policy on the 16 B vector path
+  __device__ __forceinline__ void load_ptr_hint(const T* __restrict__ p, uint64_t pol) {
+    constexpr int BYTES = VPL * (int)sizeof(T);
+    if constexpr (BYTES % 16 == 0) {
+#pragma unroll
+      for (int c = 0; c < BYTES / 16; ++c) {
+        float4 q = ld_f4_hint(reinterpret_cast<const float4*>(p) + c, pol);
+        *reinterpret_cast<float4*>(&v[c * (16 / sizeof(T))]) = q;
+      }
+    } else {
+      load_ptr(p);
+    }
+  }
+
   // gather with an L2 eviction-priority policy (16 B vector path)
   __device__ __forceinline__ void load_hint(const T* __restrict__ row, int lane, int ncols, uint64_t pol) {
     constexpr int BYTES = VPL * (int)sizeof(T);

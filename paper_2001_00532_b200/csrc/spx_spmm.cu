@@ -31,6 +31,10 @@
 
 #include "spx_common.cuh"
 
+#ifndef SPX_SPMM_MINB
+#define SPX_SPMM_MINB 3  // 512-thread blocks per SM the register path is compiled for (42 regs)
+#endif
+
 namespace spx {
 namespace {
 
@@ -96,7 +100,7 @@ struct Batch {
 //            cp.async.wait_group is the only synchronisation; no data
 //            registers are held for rows in flight, which buys occupancy.
 template <typename T, int VPL, bool CONTIG, int U, int RING>
-__global__ void __launch_bounds__(kMaxThreads) spmm_nnz_kernel(
+__global__ void __launch_bounds__(kMaxThreads, RING == 0 ? SPX_SPMM_MINB : 1) spmm_nnz_kernel(
     const int32_t* __restrict__ pos, const int32_t* __restrict__ crd, const T* __restrict__ vals,
     const T* __restrict__ B, T* __restrict__ C, int64_t M, int64_t N, int64_t nnz, int64_t TB,
     int64_t W, int32_t* __restrict__ carry_row, T* __restrict__ carry_val, const uint32_t* __restrict__ hot,
@@ -231,61 +235,63 @@ __global__ void __launch_bounds__(kMaxThreads) spmm_nnz_kernel(
       }
       cp_async_wait<0>();
     } else {
-    int nc = 0;
-    T nv = T(0);
-    if (p + lane < qe) {
-      nc = ld_i32_first(crd + p + lane, pol_s);
-      nv = ld_stream_hint(vals + p + lane, pol_s);
-    }
-    constexpr int G = 32 / U;
-    while (p < qe) {
-      const int n = min(32, qe - p);
-      const int my_c = nc;
-      const T my_v = nv;
-      if (p + 32 + lane < qe) {
-        nc = ld_i32_first(crd + p + 32 + lane, pol_s);
-        nv = ld_stream_hint(vals + p + 32 + lane, pol_s);
-      }
-      auto gather = [&](F(&buf)[U], int g) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int c = __shfl_sync(kFull, my_c, (g * U + u) & 31);
-          if (g * U + u < n) buf[u].load_hint(Bp + (int64_t)c * N, lane, ncols, pol_b);
+      // Staged-register path: the (column, value) pairs of each 32-position
+      // batch stream into a per-warp cp.async ring and come back as 16 B
+      // broadcasts (4 columns / 4 values per LDS); the B rows go straight
+      // into registers with LDG.128, four rows in flight per warp.  Per
+      // nonzero: one 512 B row gather + half a broadcast + VPL/2 FFMA2.
+      constexpr int SR = 4;  // ring depth (batches)
+      using Ring = LeafRing<T, SR>;
+      Ring ring;
+      ring.init(reinterpret_cast<unsigned char*>(ring_base) + (size_t)warp * Ring::kBytes, crd, vals, p, qe);
+      ring.prologue(lane, pol_s);
+      const char* __restrict__ Bl = reinterpret_cast<const char*>(Bp + (CONTIG ? lane * VPL : 0));
+      const uint32_t rowb = (uint32_t)(N * (int64_t)sizeof(T));
+      auto brow = [&](F& d, int c) {
+        if constexpr (CONTIG) {
+          d.load_ptr_hint(reinterpret_cast<const T*>(addr_wide(Bl, (uint32_t)c, rowb)), pol_b);
+        } else {
+          d.load(reinterpret_cast<const T*>(addr_wide(Bl, (uint32_t)c, rowb)), lane, ncols);
         }
       };
-      auto consume = [&](F(&buf)[U], int g) {
-        const int base = p + g * U;
-        const int cnt = min(U, n - g * U);
-        int u0 = 0;
-        while (true) {
-          while (base + u0 >= rend) {  // row(s) finished: store, skip empty rows
-            flush();
-            ++rr32;
-            rend = (int)ends.end(pos, rr32, M, lane);
-          }
-          const int stop = min(cnt, rend - base);
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const T v = __shfl_sync(kFull, my_v, (g * U + u) & 31);
-            if (u >= u0 && u < stop) acc.fma(v, buf[u]);
-          }
-          u0 = stop;
-          if (u0 >= cnt) break;
-        }
-      };
-      // Single buffer of U rows in registers: the gathers of one group are
-      // all in flight before the first FMA, and the SM's other warps hide
-      // the latency (occupancy instead of a second buffer: the L1TEX gather
-      // path, ~64 B/clk/SM, is the bound -- profiles/r01_gather_bound.txt)
+      for (int b = 0; b < ring.nb; ++b) {
+        ring.acquire(b, lane, pol_s);
+        const int pb = p + b * 32;
+        const int n = min(32, qe - pb);
+        const int32_t* Cs = ring.crd_slot(b);
+        const T* Vs = ring.val_slot(b);
 #pragma unroll 1
-      for (int g = 0; g < G; ++g) {
-        if (g * U >= n) break;
-        F buf[U];
-        gather(buf, g);
-        consume(buf, g);
+        for (int t = 0; t < n; t += 4) {
+          const int4 c4 = *reinterpret_cast<const int4*>(Cs + t);  // zero-filled past n
+          F b0, b1, b2, b3;
+          brow(b0, c4.x);
+          brow(b1, c4.y);
+          brow(b2, c4.z);
+          brow(b3, c4.w);
+          const T v0 = Vs[t], v1 = Vs[t + 1], v2 = Vs[t + 2], v3 = Vs[t + 3];
+          if (pb + t + 4 <= rend && t + 4 <= n) {
+            acc.fma(v0, b0);
+            acc.fma(v1, b1);
+            acc.fma(v2, b2);
+            acc.fma(v3, b3);
+          } else {
+            const F* bb[4] = {&b0, &b1, &b2, &b3};
+            const T vv[4] = {v0, v1, v2, v3};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              if (t + u < n) {
+                while (pb + t + u >= rend) {  // row(s) finished: store, skip empty rows
+                  flush();
+                  ++rr32;
+                  rend = (int)ends.end(pos, rr32, M, lane);
+                }
+                acc.fma(vv[u], *bb[u]);
+              }
+            }
+          }
+        }
+        ring.release();
       }
-      p += n;
-    }
     }  // RING == 0
     flush();
     r = rr32;
@@ -436,7 +442,7 @@ int check_bound(const Args& a, int64_t N) {
 int ring_depth() {
   static const int d = [] {
     const char* s = getenv("SPX_SPMM_RING");
-    return s ? atoi(s) : 8;
+    return s ? atoi(s) : -1;
   }();
   return d;
 }
@@ -470,9 +476,10 @@ int run_spmm(int kid, const Args& a, const SpmmGeom& g) {
     if (nnz > 0)
       if (int e = launch_chunk_segments(pos, M, W, ncta * (TB / W), first, a.stream)) return e;
     const size_t head_smem = ((size_t)nw * (g.pw * sizeof(T) + sizeof(int32_t)) + 15) & ~size_t(15);
+    const size_t reg_ring = (size_t)nw * LeafRing<T, 4>::kBytes;  // staged-register path
     dim3 grid((unsigned)ncta, (unsigned)g.npanels);
     const uint32_t* hot = nullptr;
-    // params[5]: ring depth override (0 = default, <0 = register pipeline)
+    // params[5]: B-row transport (0 = default SPX_SPMM_RING or the staged-register path, >0 = cp.async ring depth, <0 = staged-register path)
     const int ring = a.params[5] != 0 ? (a.params[5] < 0 ? 0 : a.params[5]) : ring_depth();
     if constexpr (CONTIG && (VPL * sizeof(T)) % 16 == 0) {
       if (ring > 0) {
@@ -488,11 +495,11 @@ int run_spmm(int kid, const Args& a, const SpmmGeom& g) {
                            : launch(spmm_nnz_kernel<T, VPL, CONTIG, U, 8>, 8);
         if (e) return e;
       } else {
-        spmm_nnz_kernel<T, VPL, CONTIG, U, 0><<<grid, nw * 32, head_smem, a.stream>>>(
+          spmm_nnz_kernel<T, VPL, CONTIG, U, 0><<<grid, nw * 32, head_smem + reg_ring, a.stream>>>(
             pos, crd, vals, B, C, M, N, nnz, TB, W, carry_row, carry_val, hot, first);
       }
     } else {
-      spmm_nnz_kernel<T, VPL, CONTIG, U, 0><<<grid, nw * 32, head_smem, a.stream>>>(
+      spmm_nnz_kernel<T, VPL, CONTIG, U, 0><<<grid, nw * 32, head_smem + reg_ring, a.stream>>>(
           pos, crd, vals, B, C, M, N, nnz, TB, W, carry_row, carry_val, hot, first);
     }
     count_launch();
