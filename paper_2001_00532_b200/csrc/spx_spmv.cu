@@ -98,7 +98,7 @@ struct ThreadChunk {
 
 // TPT > 0: compile-time NNZ_PER_THREAD; TPT == 0: runtime `tpt`.
 template <typename T, int TPT>
-__global__ void __launch_bounds__(kMaxThreads) spmv_nnz_kernel(const int32_t* __restrict__ pos,
+__global__ void __launch_bounds__(kMaxThreads, 2) spmv_nnz_kernel(const int32_t* __restrict__ pos,
                                                         const int32_t* __restrict__ crd,
                                                         const T* __restrict__ vals, const T* __restrict__ x,
                                                         T* __restrict__ y, int64_t M, int64_t nnz, int64_t TB,
@@ -110,14 +110,15 @@ __global__ void __launch_bounds__(kMaxThreads) spmv_nnz_kernel(const int32_t* __
   T* s_hval = reinterpret_cast<T*>(smem_raw);
   int32_t* s_hrow = reinterpret_cast<int32_t*>(s_hval + blockDim.x);
 
+  // positions are int32 (pos/crd are int32, tensors.py:248-249)
   const int tpt = TPT > 0 ? TPT : tpt_rt;
   const int tid = threadIdx.x;
-  const int64_t cta = blockIdx.x;
-  const int64_t p0 = cta * TB;
-  const int64_t p1 = min(p0 + TB, nnz);
-  const int64_t a = min(p0 + (int64_t)tid * tpt, p1);
-  const int64_t e = min(a + tpt, p1);
-  const int n = (int)(e - a);
+  const int cta = blockIdx.x;
+  const int p0 = (int)((int64_t)cta * TB);
+  const int p1 = (int)min((int64_t)p0 + TB, nnz);
+  const int a = min(p0 + tid * tpt, p1);
+  const int e = min(a + tpt, p1);
+  const int n = e - a;
 
   if (p0 >= p1) {
     if (nnz == 0 && cta == 0)
@@ -126,100 +127,160 @@ __global__ void __launch_bounds__(kMaxThreads) spmv_nnz_kernel(const int32_t* __
     return;
   }
   // Issue this thread's (crd, vals) loads and x gathers first so their
-  // latency overlaps the staging of pos below (one dependent global round
-  // trip per phase instead of a serial search chain).
-  ThreadChunk<T, (TPT > 0 ? TPT : 1)> ch;
+  // latency overlaps the staging of pos below.
+  int32_t cc[TPT > 0 ? TPT : 1];
+  T vv[TPT > 0 ? TPT : 1];
   T xv[TPT > 0 ? TPT : 1];
   if constexpr (TPT > 0) {
-    ch.load(crd, vals, a, n);
+    if (TPT % 4 == 0 && n == TPT) {
 #pragma unroll
-    for (int k = 0; k < TPT; ++k) xv[k] = k < n ? __ldg(x + ch.c[k]) : T(0);
+      for (int k = 0; k < TPT / 4; ++k) {
+        const int4 q = __ldcs(reinterpret_cast<const int4*>(crd + a) + k);
+        cc[4 * k] = q.x;
+        cc[4 * k + 1] = q.y;
+        cc[4 * k + 2] = q.z;
+        cc[4 * k + 3] = q.w;
+      }
+      if constexpr (sizeof(T) == 8) {
+#pragma unroll
+        for (int k = 0; k < TPT / 2; ++k) {
+          const double2 q = __ldcs(reinterpret_cast<const double2*>(vals + a) + k);
+          vv[2 * k] = q.x;
+          vv[2 * k + 1] = q.y;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < TPT / 4; ++k) {
+          const float4 q = __ldcs(reinterpret_cast<const float4*>(vals + a) + k);
+          vv[4 * k] = q.x;
+          vv[4 * k + 1] = q.y;
+          vv[4 * k + 2] = q.z;
+          vv[4 * k + 3] = q.w;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < TPT; ++k) {
+        cc[k] = k < n ? __ldcs(crd + a + k) : 0;
+        vv[k] = k < n ? __ldcs(vals + a + k) : T(0);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < TPT; ++k) xv[k] = __ldg(x + cc[k]);  // cc = 0 past n: harmless
   }
   // rows of this chunk: [first[cta], first[cta+1]] (chunk_segments_kernel)
-  const int64_t rlo = __ldg(first + cta), rhi = __ldg(first + cta + 1);
-  const int64_t nstage = rhi - rlo + 2;  // pos[rlo .. rhi+1]
+  const int rlo = __ldg(first + cta), rhi = __ldg(first + cta + 1);
+  const int nstage = rhi - rlo + 2;  // pos[rlo .. rhi+1]
   const bool staged = nstage <= kPosCache;
   if (staged)
-    for (int64_t k = tid; k < nstage; k += blockDim.x) s_pos[k] = __ldg(pos + rlo + k);
+    for (int k = tid; k < nstage; k += blockDim.x) s_pos[k] = __ldg(pos + rlo + k);
   __syncthreads();
-  auto P = [&](int64_t r) -> int64_t {  // pos[r] for r in [rlo, rhi+1]
-    return staged ? (int64_t)s_pos[r - rlo] : (int64_t)__ldg(pos + r);
-  };
+#define SPX_P(r) (staged ? s_pos[(r) - rlo] : __ldg(pos + (r)))
 
   int32_t head = -1;
   T hval = T(0);
-  if (a < e) {
+  if (n > 0) {
     // SearchSegment over the CTA's rows (ir.py:178-190)
-    int64_t lo = rlo, hi = rhi + 1;
+    int lo = rlo, hi = rhi + 1;
     while (lo < hi) {
-      int64_t mid = (lo + hi) >> 1;
-      if (P(mid) <= a) lo = mid + 1;
+      const int mid = (lo + hi) >> 1;
+      if (SPX_P(mid) <= a) lo = mid + 1;
       else hi = mid;
     }
-    int64_t r = lo - 1;
-    bool is_head = P(r) < a;
+    int r = lo - 1;
+    bool is_head = SPX_P(r) < a;
     if (!is_head && r > 0) {
       // empty rows with pos == a before r are owned by this thread
-      int64_t rr = r - 1;
-      while (rr >= rlo && P(rr) == a) __stcs(y + rr--, T(0));
+      int rr = r - 1;
+      while (rr >= rlo && SPX_P(rr) == a) __stcs(y + rr--, T(0));
       if (rr < rlo && rr >= 0 && __ldg(pos + rr) == a) {
-        int64_t lb = lower_bound(pos, 0, rlo, a);
-        for (int64_t q = lb; q < rlo; ++q) __stcs(y + q, T(0));
+        const int lb = (int)lower_bound(pos, 0, rlo, a);
+        for (int q = lb; q < rlo; ++q) __stcs(y + q, T(0));
       }
     }
-    int64_t rend = P(r + 1);
+    int rend = SPX_P(r + 1);
     T acc = T(0);
-    auto step = [&](int64_t p, T prod) {
-      while (p >= rend) {
-        if (is_head) {
-          head = (int32_t)r;
-          hval = acc;
-          is_head = false;
-        } else {
-          __stcs(y + r, acc);
-        }
-        acc = T(0);
-        ++r;
-        rend = P(r + 1);
-      }
-      acc += prod;
-    };
     if constexpr (TPT > 0) {
       if (n == TPT && a + TPT <= rend) {
         // whole chunk inside one row: plain fold, no tracking
 #pragma unroll
-        for (int k = 0; k < TPT; ++k) acc += ch.v[k] * xv[k];
+        for (int k = 0; k < TPT; ++k) acc += vv[k] * xv[k];
       } else {
 #pragma unroll
-        for (int k = 0; k < TPT; ++k)
-          if (k < n) step(a + k, ch.v[k] * xv[k]);
+        for (int k = 0; k < TPT; ++k) {
+          if (k < n) {
+            while (a + k >= rend) {
+              if (is_head) {
+                head = r;
+                hval = acc;
+                is_head = false;
+              } else {
+                __stcs(y + r, acc);
+              }
+              acc = T(0);
+              ++r;
+              rend = SPX_P(r + 1);
+            }
+            acc += vv[k] * xv[k];
+          }
+        }
       }
     } else {
-      for (int64_t p = a; p < e; ++p) step(p, __ldcs(vals + p) * __ldg(x + __ldcs(crd + p)));
+      for (int p = a; p < e; ++p) {
+        const T prod = __ldcs(vals + p) * __ldg(x + __ldcs(crd + p));
+        while (p >= rend) {
+          if (is_head) {
+            head = r;
+            hval = acc;
+            is_head = false;
+          } else {
+            __stcs(y + r, acc);
+          }
+          acc = T(0);
+          ++r;
+          rend = SPX_P(r + 1);
+        }
+        acc += prod;
+      }
     }
     if (is_head) {
-      head = (int32_t)r;
+      head = r;
       hval = acc;
     } else {
       __stcs(y + r, acc);
     }
     if (e == nnz)
-      for (int64_t q = r + 1; q < M; ++q) __stcs(y + q, T(0));
+      for (int64_t q = (int64_t)r + 1; q < M; ++q) __stcs(y + q, T(0));
   }
+  // Fold the head partials: threads with equal head rows are contiguous in
+  // tid order.  Segmented shuffle reduction inside each warp (the first lane
+  // of a run ends with the run's warp-local sum), then runs that cross warps
+  // are joined through one partial per warp.
+  const int lane = tid & 31, warp = tid >> 5;
+  T hv = hval;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const T y = __shfl_down_sync(kFull, hv, o);
+    const int h2 = __shfl_down_sync(kFull, head, o);
+    if (lane + o < 32 && h2 == head) hv += y;
+  }
+  const int hprev = __shfl_up_sync(kFull, head, 1);
   s_hrow[tid] = head;
-  s_hval[tid] = hval;
+  if (lane == 0) s_hval[warp] = hv;  // the lane-0 run's warp-local sum
   __syncthreads();
-  if (head >= 0 && (tid == 0 || s_hrow[tid - 1] != head)) {
-    T s = hval;
-    for (int t2 = tid + 1; t2 < (int)blockDim.x && s_hrow[t2] == head; ++t2) s += s_hval[t2];
-    if (P(head) >= p0) {
+  if (head >= 0 && (lane == 0 || hprev != head) && (tid == 0 || s_hrow[tid - 1] != head)) {
+    T s = hv;
+    const int nw = blockDim.x >> 5;
+    for (int w2 = warp + 1; w2 < nw && s_hrow[w2 * 32] == head; ++w2) s += s_hval[w2];
+    if (SPX_P(head) >= p0) {
       y[head] = __ldcg(y + head) + s;
     } else {
       carry_val[cta] = s;
       carry_row[cta] = head;
     }
   }
-  if (tid == 0 && !(head >= 0 && P(head) < p0)) carry_row[cta] = -1;
+  if (tid == 0 && !(head >= 0 && SPX_P(head) < p0)) carry_row[cta] = -1;
+#undef SPX_P
 }
 
 template <typename T>

@@ -133,6 +133,27 @@ __global__ void __launch_bounds__(256) g_tma(const int* __restrict__ cols, long 
   out[w * 32 + lane] = acc;
 }
 
+// ---- path 3: 8 B scalar gathers (SpMV x[crd[p]]), 8 per thread ---------------
+__global__ void __launch_bounds__(256) g_scalar(const int* __restrict__ cols, long n, const double* __restrict__ x,
+                                                double* __restrict__ out) {
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long a = t * 8;
+  double acc = 0.0;
+  if (a + 8 <= n) {
+    const int4 c0 = __ldcs(reinterpret_cast<const int4*>(cols + a));
+    const int4 c1 = __ldcs(reinterpret_cast<const int4*>(cols + a) + 1);
+    acc = __ldg(x + c0.x) + __ldg(x + c0.y) + __ldg(x + c0.z) + __ldg(x + c0.w) + __ldg(x + c1.x) +
+          __ldg(x + c1.y) + __ldg(x + c1.z) + __ldg(x + c1.w);
+  }
+  out[t] = acc;
+}
+
+extern "C" int gb2_scalar(const int* cols, long n, const void* x, void* out, void* stream) {
+  const long threads = n / 8;
+  g_scalar<<<(threads + 255) / 256, 256, 0, (cudaStream_t)stream>>>(cols, n, (const double*)x, (double*)out);
+  return (int)cudaGetLastError();
+}
+
 extern "C" int gb2_gather(int path, const int* cols, long n, const void* B, void* out, long per_warp, int variant,
                           void* stream) {
   cudaStream_t s = (cudaStream_t)stream;

@@ -29,7 +29,29 @@ def build():
     lib = ctypes.CDLL(str(SO))
     lib.gb2_gather.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_long, ctypes.c_void_p, ctypes.c_void_p,
                                ctypes.c_long, ctypes.c_int, ctypes.c_void_p]
+    lib.gb2_scalar.argtypes = [ctypes.c_void_p, ctypes.c_long, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
     return lib
+
+
+def scalar_main(lib):
+    """8 B gathers of x (cfg5: 4,194,304 doubles = 33.5 MB) over cfg5's column stream."""
+    from paper_2001_00532_b200 import synth
+
+    dev = torch.device("cuda:0")
+    stream = torch.cuda.current_stream().cuda_stream
+    A = synth.config_matrix(5)
+    n = A.nnz
+    x = torch.rand(A.N, dtype=torch.float64, device=dev)
+    out = torch.empty(n // 8 + 256, dtype=torch.float64, device=dev)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    for name, cols in {"cfg5 crd": torch.from_numpy(A.crd).to(dev),
+                       "sequential": torch.arange(n, dtype=torch.int32, device=dev) % A.N,
+                       "uniform random": torch.randint(0, A.N, (n,), device=dev, dtype=torch.int32)}.items():
+        fn = lambda: lib.gb2_scalar(cols.data_ptr(), n, x.data_ptr(), out.data_ptr(), stream)
+        fn()
+        torch.cuda.synchronize()
+        t, tm = timeit(fn, flush)
+        print(f"scalar 8B gathers, {name:16s}: {t:.3f} ms (med {tm:.3f}) -> {n / t / 1e6:.1f} G gathers/s", flush=True)
 
 
 def timeit(fn, flush, reps=7):
@@ -76,4 +98,7 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if "--scalar" in sys.argv:
+        scalar_main(build())
+    else:
+        main()
