@@ -132,15 +132,24 @@ __global__ void partition_kernel(const int32_t* __restrict__ seg_start, int64_t 
 
 __global__ void chunk_segments_kernel(const int32_t* __restrict__ pos, int64_t nseg, int64_t chunk, int64_t nchunks,
                                       int32_t* __restrict__ first) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nseg; r += stride) {
-    const int64_t a = __ldcs(pos + r), e = __ldcs(pos + r + 1);
+  // positions are int32 (tensors.py:248-249): 32-bit arithmetic throughout
+  const uint32_t ch = (uint32_t)chunk;
+  const int stride = (int)(gridDim.x * blockDim.x);
+  for (int r = (int)(blockIdx.x * blockDim.x + threadIdx.x); r < (int)nseg; r += stride) {
+    const uint32_t a = (uint32_t)__ldcs(pos + r), e = (uint32_t)__ldcs(pos + r + 1);
+    if (a == e) continue;
     // chunks c with a <= c*chunk < e start inside segment r; later segments
     // start after e and earlier ones end at or before a, so r is the largest
     // segment with pos[r] <= c*chunk
-    for (int64_t c = (a + chunk - 1) / chunk; c * chunk < e; ++c) first[c] = (int32_t)r;
+    for (uint32_t c = (a + ch - 1) / ch; (uint64_t)c * ch < e; ++c) first[c] = r;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) first[nchunks] = (int32_t)(nseg > 0 ? nseg - 1 : 0);
+  // chunks starting at or past the last position (and the sentinel entry
+  // nchunks) map to the last segment
+  if (blockIdx.x == 0) {
+    const int64_t nnz = nseg > 0 ? (int64_t)__ldg(pos + nseg) : 0;
+    for (int64_t c = (nnz + chunk - 1) / chunk + threadIdx.x; c <= nchunks; c += blockDim.x)
+      first[c] = (int32_t)(nseg > 0 ? nseg - 1 : 0);
+  }
 }
 
 int launch_chunk_segments(const int32_t* pos, int64_t nseg, int64_t chunk, int64_t nchunks, int32_t* first,

@@ -62,7 +62,8 @@ inline NnzWorkspace nnz_workspace(int64_t ncta, size_t es, int64_t vals_per_cta 
 // first[c] = SearchSegment(pos, 0, nseg, c*chunk) (ir.py:178-190) for every
 // chunk c in [0, nchunks) of `chunk` consecutive leaf positions, computed by
 // one coalesced pass over pos (each nonempty segment writes the chunks whose
-// first position it holds); first[nchunks] = nseg - 1.  Replaces a serial
+// first position it holds); chunks at or past the last position and the
+// sentinel first[nchunks] get nseg - 1.  Replaces a serial
 // binary search at the start of every CTA/warp of the nnz-split kernels.
 int launch_chunk_segments(const int32_t* pos, int64_t nseg, int64_t chunk, int64_t nchunks, int32_t* first,
                           cudaStream_t stream);
