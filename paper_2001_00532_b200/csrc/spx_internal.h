@@ -40,6 +40,7 @@ int launch_csf(int kernel_id, const Args& a);
 size_t ws_spmv(int kernel_id, const Args& a);
 size_t ws_spmm(int kernel_id, const Args& a);
 size_t ws_csf(int kernel_id, const Args& a);
+size_t ws_sddmm(int kernel_id, const Args& a);
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 

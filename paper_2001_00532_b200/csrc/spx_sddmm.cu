@@ -100,29 +100,109 @@ __device__ __forceinline__ void sddmm_batch(const int32_t* __restrict__ pos, con
   if (lane < n) emit(out, dense, N, p + lane, my_r, my_c, my_v * s);
 }
 
+// part[i] (i < 8) on every lane -> lanes with (lane & 3) == 0 hold the sum
+// over all lanes of part[lane >> 2]: 3 halving exchange steps + 2 folds.
+template <typename T>
+__device__ __forceinline__ T transpose_reduce8(T (&part)[8], int lane) {
+#pragma unroll
+  for (int o = 16, h = 4; o >= 4; o >>= 1, h >>= 1) {
+    const bool upper = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < h; ++i) {
+      const T send = upper ? part[i] : part[i + h];
+      const T keep = upper ? part[i + h] : part[i];
+      part[i] = keep + __shfl_xor_sync(kFull, send, o);
+    }
+  }
+  T v = part[0];
+  v += __shfl_xor_sync(kFull, v, 2);
+  v += __shfl_xor_sync(kFull, v, 1);
+  return v;
+}
+
+// K6: warp chunk q covers positions [q*W, q*W+W).  The (column, value) pairs
+// stream through a per-warp cp.async ring; the warp takes the chunk eight
+// positions at a time: U rows of D in flight, each dotted with the current
+// C row (held in registers while the row lasts), the eight partial dot
+// products folded by transpose_reduce8, and the 32 results of a batch
+// stored coalesced by the lanes that own them.
 template <typename T, int VPL, bool CONTIG, int U>
-__global__ void __launch_bounds__(kMaxThreads) sddmm_nnz_kernel(const int32_t* __restrict__ pos,
-                                                         const int32_t* __restrict__ crd,
-                                                         const T* __restrict__ vals, const T* __restrict__ Cm,
-                                                         const T* __restrict__ Dm, T* __restrict__ out, int64_t M,
-                                                         int64_t N, int64_t K, int64_t nnz, int64_t TB, int64_t W,
-                                                         bool dense) {
+__global__ void __launch_bounds__(kMaxThreads, 2) sddmm_nnz_kernel(const int32_t* __restrict__ pos,
+                                                            const int32_t* __restrict__ crd,
+                                                            const T* __restrict__ vals, const T* __restrict__ Cm,
+                                                            const T* __restrict__ Dm, T* __restrict__ out, int64_t M,
+                                                            int64_t N, int64_t K, int64_t nnz, int64_t W,
+                                                            int wpc, bool dense, const int32_t* __restrict__ first) {
+  using F = Frag<T, VPL, CONTIG>;
+  using Ring = LeafRing<T, 4>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t p0 = (int64_t)blockIdx.x * TB;
-  const int64_t p1 = min(p0 + TB, nnz);
-  const int64_t q0 = min(p0 + (int64_t)warp * W, p1);
-  const int64_t q1 = min(q0 + W, p1);
+  const int q = (int)blockIdx.x * wpc + warp;
+  const int q0 = (int)((int64_t)q * W);
+  const int q1 = (int)min((int64_t)q0 + W, nnz);
   if (q0 >= q1) return;
-  int64_t r = warp_search_segment(pos, 0, M, q0, lane);
+  const int ncols = (int)K;
+  const uint64_t pol_s = l2_evict_first();
+  int64_t r = __ldg(first + q);  // row holding q0 (chunk_segments_kernel)
   RowEndCache ends;
   ends.fill(pos, r, M, lane);
-  int64_t rend = ends.end(pos, r, M, lane);
-  Frag<T, VPL, CONTIG> crow;
-  crow.load(Cm + r * K, lane, (int)K);
-  for (int64_t p = q0; p < q1; p += 32) {
-    const int n = (int)min((int64_t)32, q1 - p);
-    sddmm_batch<T, VPL, CONTIG, U, false>(pos, crd, vals, Cm, Dm, out, M, N, K, dense, p, n, r, rend, ends, crow,
-                                          lane);
+  int rend = (int)ends.end(pos, r, M, lane);
+  F crow;
+  crow.load(Cm + r * K, lane, ncols);
+  const char* __restrict__ Dl = reinterpret_cast<const char*>(Dm + (CONTIG ? lane * VPL : lane));
+  const uint32_t rowb = (uint32_t)(K * (int64_t)sizeof(T));
+  auto drow = [&](F& d, int c) {
+    const T* src = reinterpret_cast<const T*>(addr_wide(Dl, (uint32_t)c, rowb));
+    if constexpr (CONTIG) {
+      d.load_ptr(src);
+    } else {
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) d.v[i] = (i * 32 + lane < ncols) ? __ldg(src + i * 32) : T(0);
+    }
+  };
+  Ring ring;
+  ring.init(smem_raw + (size_t)warp * Ring::kBytes, crd, vals, q0, q1);
+  ring.prologue(lane, pol_s);
+  for (int b = 0; b < ring.nb; ++b) {
+    ring.acquire(b, lane, pol_s);
+    const int p = q0 + b * 32;
+    const int n = min(32, q1 - p);
+    const int32_t* Cs = ring.crd_slot(b);
+    const T* Vs = ring.val_slot(b);
+    T res = T(0);
+    int64_t myr = r;  // row of position p + lane (dense scatter)
+#pragma unroll 1
+    for (int g = 0; g < 4 && g * 8 < n; ++g) {
+      T part[8];
+#pragma unroll
+      for (int u0 = 0; u0 < 8; u0 += U) {
+        F d[U];
+#pragma unroll
+        for (int uu = 0; uu < U; ++uu) drow(d[uu], Cs[g * 8 + u0 + uu]);  // zero-filled past n
+#pragma unroll
+        for (int uu = 0; uu < U; ++uu) {
+          const int t = g * 8 + u0 + uu;
+          if (t < n) {
+            if (p + t >= rend) {
+              do {
+                ++r;
+                rend = (int)ends.end(pos, r, M, lane);
+              } while (p + t >= rend);
+              crow.load(Cm + r * K, lane, ncols);
+            }
+            if (lane == t) myr = r;
+            part[u0 + uu] = dot(crow, d[uu]);
+          } else {
+            part[u0 + uu] = T(0);
+          }
+        }
+      }
+      const T sum = transpose_reduce8(part, lane);
+      const T got = __shfl_sync(kFull, sum, (lane & 7) * 4);
+      if ((lane >> 3) == g) res = got;
+    }
+    if (lane < n) emit(out, dense, N, (int64_t)p + lane, myr, Cs[lane], Vs[lane] * res);
+    ring.release();
   }
 }
 
@@ -178,8 +258,15 @@ int run_sddmm(int kid, const Args& a) {
     const int64_t TB = a.params[0], W = a.params[1];
     if (TB < 1 || W < 1 || TB % W != 0 || TB / W > kMaxWarps)
       return fail(SPX_E_UNSUPPORTED, "SDDMM nnz-split needs NNZ_PER_TB a multiple of NNZ_PER_WARP, <= 16 warps");
-    sddmm_nnz_kernel<T, VPL, CONTIG, U><<<(unsigned)ceil_div(nnz, TB), (unsigned)(TB / W * 32), 0, a.stream>>>(
-        pos, crd, vals, Cm, Dm, out, M, N, K, nnz, TB, W, dense);
+    const int64_t wpc = TB / W, ncta = ceil_div(nnz, TB), nchunks = ncta * wpc;
+    if (!a.ws || a.ws_bytes < (size_t)(nchunks + 1) * sizeof(int32_t))
+      return fail(SPX_E_WORKSPACE, "workspace %zu < %zu bytes", a.ws_bytes, (size_t)(nchunks + 1) * 4);
+    int32_t* first = static_cast<int32_t*>(a.ws);
+    if (int e = launch_chunk_segments(pos, M, W, nchunks, first, a.stream)) return e;
+    constexpr int UN = VPL * (int)sizeof(T) >= 32 ? 2 : 4;  // D rows in flight per warp
+    sddmm_nnz_kernel<T, VPL, CONTIG, UN><<<(unsigned)ncta, (unsigned)(wpc * 32), wpc * LeafRing<T, 4>::kBytes,
+                                           a.stream>>>(pos, crd, vals, Cm, Dm, out, M, N, K, nnz, W, (int)wpc,
+                                                       dense, first);
     count_launch();
     return check_cuda(cudaGetLastError(), "sddmm_nnz_kernel");
   }
@@ -214,6 +301,15 @@ int dispatch_sddmm(int kid, const Args& a, int64_t K) {
 }
 
 }  // namespace
+
+size_t ws_sddmm(int kid, const Args& a) {
+  if (kid != SPX_K_SDDMM_NNZ) return 0;
+  const int64_t nnz = a.level_sizes[1];
+  const int64_t TB = a.params[0] > 0 ? a.params[0] : 1;
+  const int64_t W = a.params[1] > 0 ? a.params[1] : TB;
+  const int64_t nchunks = ceil_div(nnz > 0 ? nnz : 1, TB) * (TB / W > 0 ? TB / W : 1);
+  return (size_t)(nchunks + 1) * sizeof(int32_t);
+}
 
 int launch_sddmm(int kid, const Args& a) {
   const int64_t M = a.dims[0][0], N = a.dims[0][1], K = a.dims[1][1];
