@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--ncols", type=int, default=128)
     ap.add_argument("--tb", type=int, default=4096, help="NNZ_PER_TB")
     ap.add_argument("--warp", type=int, default=512, help="NNZ_PER_WARP")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no clock loop / e2e / cpu leg")
@@ -282,7 +282,11 @@ def main():
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
             "frac": round(achieved / hbm, 4), "traffic": load_traffic(), "peak_kind": peak_kind,
             "kernel": "spmm_nnz_kernel + carry_fixup_kernel (one spx_launch)",
-            "algorithmic_bytes_per_launch": cb_local}
+            "algorithmic_bytes_per_launch": cb_local,
+            # what binds this kernel: every nonzero gathers one N-wide row of B
+            # from L2; the L2->SM rate achieved on it
+            "gathered_bytes_per_launch": int(nnz_local * N * 4),
+            "gather_TBs": round(nnz_local * N * 4 / (statistics.mean(times) * 1e-3) / 1e12, 2)}
 
     # gather of the sharded output (reported separately)
     gather_ms = None
@@ -298,10 +302,13 @@ def main():
         gather_ms = (time.perf_counter() - g0) * 1e3
         del full
 
-    # e2e through the public API with pinned host inputs
+    # e2e through the public API with pinned host inputs: every step uploads
+    # A and B, runs the launch and downloads C.  `Pipeline` overlaps step
+    # k+1's upload with step k's kernel and download (full-duplex PCIe);
+    # `interpret` (one synchronous step) is reported beside it.
     e2e = None
     if world == 1 and args.e2e_steps > 0 and not args.profile:
-        from paper_2001_00532_b200._spindle import tensors as T
+        from paper_2001_00532_b200.pipeline import Pipeline
 
         hA = DeviceTensor.from_arrays((A.M, A.N), "ds", {1: A.pos}, {1: A.crd}, A.vals32, dtype="f32", pin=True)
         hB = DeviceTensor.dense(B, dtype="f32", pin=True)
@@ -315,13 +322,29 @@ def main():
             t0 = time.perf_counter()
             interpret(prog, {"A": hA, "B": hB}, out=hout)  # H2D + launch + D2H + sync
             ts.append(time.perf_counter() - t0)
-        e_t = statistics.median(ts)
-        e2e = {"value": round(flops / e_t / 1e9, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e_t * 1e3, 3)}
-        # parity spot check of the e2e result against the device result
+        sync_t = statistics.median(ts)
+        # parity spot check of the synchronous e2e result against the device path
         ex.launch()
         torch.cuda.synchronize(dev)
         assert torch.equal(hout.view(-1), out.cpu().view(-1)), "e2e result differs from the device path"
+        del ex, out  # free HBM for the pipeline's two slots
+        torch.cuda.empty_cache()
+        pipe = Pipeline(prog, {"A": hA, "B": hB}, hout, dtype="f32", depth=2, device=dev)
+        pipe.submit({"A": hA, "B": hB}, hout)  # warm
+        pipe.drain()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            pipe.submit({"A": hA, "B": hB}, hout)
+        pipe.drain()
+        e_t = (time.perf_counter() - t0) / args.e2e_steps
+        e2e = {"value": round(flops / e_t / 1e9, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e_t * 1e3, 3),
+               "api": f"Pipeline(depth=2): {args.e2e_steps} steps, host wall clock / steps",
+               "sync_interpret": {"value": round(flops / sync_t / 1e9, 3), "ms_per_step": round(sync_t * 1e3, 3)}}
+        ref = torch.empty_like(hout)
+        interpret(prog, {"A": hA, "B": hB}, out=ref)
+        assert torch.equal(hout.view(-1), ref.view(-1)), "pipelined e2e result differs from interpret"
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and not args.profile:

@@ -32,7 +32,7 @@
 #include "spx_common.cuh"
 
 #ifndef SPX_SPMM_MINB
-#define SPX_SPMM_MINB 3  // 512-thread blocks per SM the register path is compiled for (42 regs)
+#define SPX_SPMM_MINB 2  // 512-thread blocks per SM the register path is compiled for (<= 64 regs, no spills)
 #endif
 
 namespace spx {

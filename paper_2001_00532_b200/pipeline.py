@@ -1,0 +1,107 @@
+"""Overlapped host -> HBM -> host execution of a lowered statement.
+
+`interpret` is synchronous: copy the step's inputs to the
+device, launch, copy the result back, return.  A caller that evaluates the
+same statement over a stream of host-resident inputs (one sparse operand
+per step, or the same operands re-sent every step) can instead hand the
+steps to a `Pipeline`: each step's host->device copies, kernel launch and
+device->host copy are queued on three CUDA streams over `depth` device
+slots, so step k+1's upload overlaps step k's kernel and step k's download
+(PCIe is full duplex; the copy engines and the SMs run concurrently).  The
+results are bit-identical to `interpret` -- the same Executor launches the
+same kernels on the same data -- only the copies overlap.
+
+Host buffers must be pinned (`DeviceTensor.from_arrays(..., pin=True)`,
+`torch.empty(...).pin_memory()`), as for any asynchronous copy.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _spindle
+from .execution import Executor
+from .formats import DeviceTensor, torch_dtype
+from .lowering import Program
+
+
+def _empty_like_on(t: DeviceTensor, device) -> DeviceTensor:
+    def e(x: torch.Tensor) -> torch.Tensor:
+        return torch.empty_like(x, device=device)
+
+    return DeviceTensor(dims=t.dims, levels=t.levels, pos={k: e(v) for k, v in t.pos.items()},
+                        crd={k: e(v) for k, v in t.crd.items()}, vals=e(t.vals))
+
+
+def _copy_into(dst: DeviceTensor, src: DeviceTensor) -> int:
+    n = 0
+    for k, v in src.pos.items():
+        dst.pos[k].copy_(v, non_blocking=True)
+        n += v.numel() * v.element_size()
+    for k, v in src.crd.items():
+        dst.crd[k].copy_(v, non_blocking=True)
+        n += v.numel() * v.element_size()
+    dst.vals.copy_(src.vals, non_blocking=True)
+    return n + src.vals.numel() * src.vals.element_size()
+
+
+class Pipeline:
+    """`depth` device slots, each an Executor bound to its own operand and
+    output buffers, fed through an upload stream, a compute stream and a
+    download stream."""
+
+    def __init__(self, program: Program, like: dict, out_like: torch.Tensor, *, dtype: str, depth: int = 2,
+                 device=None):
+        E = _spindle.errors
+        if not torch.cuda.is_available():
+            raise E.ExecutionError("Pipeline needs a CUDA device (there is no CPU fallback)")
+        self.device = torch.device(device or "cuda")
+        self.depth = max(1, int(depth))
+        self.program = program
+        self.slots = []
+        for _ in range(self.depth):
+            ops = {name: _empty_like_on(t, self.device) for name, t in like.items()}
+            out = torch.empty(out_like.numel(), dtype=torch_dtype(dtype), device=self.device)
+            self.slots.append((ops, out, Executor(program, ops, out, dtype=dtype)))
+        self.up = torch.cuda.Stream(self.device)
+        self.compute = torch.cuda.Stream(self.device)
+        self.down = torch.cuda.Stream(self.device)
+        self.free = [None] * self.depth  # event: slot's previous download finished
+        self.k = 0
+        self.h2d_bytes = 0
+        self.d2h_bytes = 0
+
+    def submit(self, inputs: dict, out: torch.Tensor) -> torch.cuda.Event:
+        """Queue one step: upload `inputs` (host DeviceTensors, pinned), run,
+        download into `out` (pinned host tensor).  Returns the event that
+        marks the step's download complete."""
+        s = self.k % self.depth
+        ops, dev_out, ex = self.slots[s]
+        with torch.cuda.stream(self.up):
+            if self.free[s] is not None:
+                self.up.wait_event(self.free[s])
+            nb = 0
+            for name, t in inputs.items():
+                nb += _copy_into(ops[name], t)
+            uploaded = torch.cuda.Event()
+            uploaded.record(self.up)
+        self.compute.wait_event(uploaded)
+        ex.launch(self.compute.cuda_stream)
+        done = torch.cuda.Event()
+        done.record(self.compute)
+        with torch.cuda.stream(self.down):
+            self.down.wait_event(done)
+            out.view(-1).copy_(dev_out, non_blocking=True)
+            fin = torch.cuda.Event()
+            fin.record(self.down)
+        # the upload stream must not overwrite this slot's device buffers
+        # before its result has been read back
+        self.free[s] = fin
+        self.h2d_bytes = nb
+        self.d2h_bytes = dev_out.numel() * dev_out.element_size()
+        self.k += 1
+        return fin
+
+    def drain(self) -> None:
+        for st in (self.up, self.compute, self.down):
+            st.synchronize()
