@@ -72,6 +72,7 @@ extern "C" {
  *  1   SpMV row-split            y(i)=A(i,j)*x(j)  A:ds   [0]=ROWS_PER_TB
  *  2   SpMV warp-per-row         "                        [0]=ROWS_PER_TB [1]=WARPS_PER_TB
  *  3   SpMV nnz-split            "                        [0]=NNZ_PER_TB [1]=NNZ_PER_WARP [2]=NNZ_PER_THREAD
+ *                                                         [5]=output strategy: 0 = Atomics (default; y zeroed, red.add), 1 = deterministic carry fix-up
  *  4   SpMM nnz-split            C(i,k)=A(i,j)*B(j,k)     [0]=NNZ_PER_TB [1]=NNZ_PER_WARP [2]=WARP_SIZE [3]=bound (0 = none)
  *                                                         [5]=B-row transport: 0 = default (staged-register path), >0 = cp.async row ring of that depth, <0 = staged-register path
  *  5   SpMM warp-per-row         "                        [0]=ROWS_PER_TB [1]=WARPS_PER_TB [2]=WARP_SIZE [3]=bound

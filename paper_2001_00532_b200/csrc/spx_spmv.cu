@@ -283,6 +283,158 @@ __global__ void __launch_bounds__(kMaxThreads, 2) spmv_nnz_kernel(const int32_t*
 #undef SPX_P
 }
 
+// Atomics variant of K3 (the default): the schedule tags `thread` with the
+// Atomics race strategy, and that is what this kernel does -- y is zeroed
+// first, a row that lies inside one thread's positions is stored plainly,
+// every other partial is added with red.global.add after a segmented
+// shuffle fold inside the warp (one atomic per row run per warp).  Warps are
+// independent: each stages the pos entries of its own rows in warp-private
+// shared memory (chunk table at NNZ_PER_WARP granularity), so there is no
+// CTA barrier and no carry fix-up.  fp64 sums of a row split across warps
+// may differ in the last bits from run to run (atomic order).
+constexpr int kWarpPos = 320;  // pos entries staged per warp
+
+template <typename T, int TPT>
+__global__ void __launch_bounds__(kMaxThreads, 2) spmv_nnz_atomic_kernel(
+    const int32_t* __restrict__ pos, const int32_t* __restrict__ crd, const T* __restrict__ vals,
+    const T* __restrict__ x, T* __restrict__ y, int64_t M, int64_t nnz, int64_t W, int tpt_rt,
+    const int32_t* __restrict__ first) {
+  __shared__ int32_t s_pos_all[kMaxWarps][kWarpPos];
+  const int tpt = TPT > 0 ? TPT : tpt_rt;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int32_t* s_pos = s_pos_all[warp];
+  const int q = (int)blockIdx.x * (int)(blockDim.x >> 5) + warp;  // warp chunk
+  const int q0 = (int)((int64_t)q * W);
+  if ((int64_t)q0 >= nnz) return;
+  const int q1 = (int)min((int64_t)q0 + W, nnz);
+  const int a = min(q0 + lane * tpt, q1);
+  const int e = min(a + tpt, q1);
+  const int n = e - a;
+  // loads first: (crd, vals) with 16 B vectors, then the x gathers
+  int32_t cc[TPT > 0 ? TPT : 1];
+  T vv[TPT > 0 ? TPT : 1];
+  T xv[TPT > 0 ? TPT : 1];
+  if constexpr (TPT > 0) {
+    if (TPT % 4 == 0 && n == TPT) {
+#pragma unroll
+      for (int k = 0; k < TPT / 4; ++k) {
+        const int4 qq = __ldcs(reinterpret_cast<const int4*>(crd + a) + k);
+        cc[4 * k] = qq.x;
+        cc[4 * k + 1] = qq.y;
+        cc[4 * k + 2] = qq.z;
+        cc[4 * k + 3] = qq.w;
+      }
+      if constexpr (sizeof(T) == 8) {
+#pragma unroll
+        for (int k = 0; k < TPT / 2; ++k) {
+          const double2 qq = __ldcs(reinterpret_cast<const double2*>(vals + a) + k);
+          vv[2 * k] = qq.x;
+          vv[2 * k + 1] = qq.y;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < TPT / 4; ++k) {
+          const float4 qq = __ldcs(reinterpret_cast<const float4*>(vals + a) + k);
+          vv[4 * k] = qq.x;
+          vv[4 * k + 1] = qq.y;
+          vv[4 * k + 2] = qq.z;
+          vv[4 * k + 3] = qq.w;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < TPT; ++k) {
+        cc[k] = k < n ? __ldcs(crd + a + k) : 0;
+        vv[k] = k < n ? __ldcs(vals + a + k) : T(0);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < TPT; ++k) xv[k] = __ldg(x + cc[k]);  // cc = 0 past n: harmless
+  }
+  const int rlo = __ldg(first + q), rhi = __ldg(first + q + 1);
+  const int nstage = rhi - rlo + 2;  // pos[rlo .. rhi+1]
+  const bool staged = nstage <= kWarpPos;
+  if (staged)
+    for (int k = lane; k < nstage; k += 32) s_pos[k] = __ldg(pos + rlo + k);
+  __syncwarp();
+#define SPX_P(r) (staged ? s_pos[(r) - rlo] : __ldg(pos + (r)))
+  int32_t head = -1;
+  T hval = T(0);
+  if (n > 0) {
+    int lo = rlo, hi = rhi + 1;  // SearchSegment (ir.py:178-190)
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (SPX_P(mid) <= a) lo = mid + 1;
+      else hi = mid;
+    }
+    int r = lo - 1;
+    bool is_head = SPX_P(r) < a;
+    int rend = SPX_P(r + 1);
+    T acc = T(0);
+    // a finished row partial: plain store when the row lies inside this
+    // thread's positions, else it joins the head fold / an atomic add
+    auto close_row = [&]() {
+      if (is_head) {
+        head = r;
+        hval = acc;
+        is_head = false;
+      } else {
+        __stcs(y + r, acc);
+      }
+    };
+    if constexpr (TPT > 0) {
+      if (n == TPT && a + TPT <= rend) {
+#pragma unroll
+        for (int k = 0; k < TPT; ++k) acc += vv[k] * xv[k];
+      } else {
+#pragma unroll
+        for (int k = 0; k < TPT; ++k) {
+          if (k < n) {
+            while (a + k >= rend) {
+              close_row();
+              acc = T(0);
+              ++r;
+              rend = SPX_P(r + 1);
+            }
+            acc += vv[k] * xv[k];
+          }
+        }
+      }
+    } else {
+      for (int p = a; p < e; ++p) {
+        const T prod = __ldcs(vals + p) * __ldg(x + __ldcs(crd + p));
+        while (p >= rend) {
+          close_row();
+          acc = T(0);
+          ++r;
+          rend = SPX_P(r + 1);
+        }
+        acc += prod;
+      }
+    }
+    // last row of the range: complete here, or shared with later threads
+    if (is_head) {
+      head = r;
+      hval = acc;
+    } else if (rend <= e) {
+      __stcs(y + r, acc);
+    } else {
+      atomicAdd(y + r, acc);
+    }
+  }
+  // segmented fold of the head partials (equal heads are contiguous lanes)
+  T hv = hval;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const T yv = __shfl_down_sync(kFull, hv, o);
+    const int h2 = __shfl_down_sync(kFull, head, o);
+    if (lane + o < 32 && h2 == head) hv += yv;
+  }
+  const int hprev = __shfl_up_sync(kFull, head, 1);
+  if (head >= 0 && (lane == 0 || hprev != head)) atomicAdd(y + head, hv);
+#undef SPX_P
+}
+
 template <typename T>
 __global__ void spmv_fixup_kernel(const int32_t* __restrict__ carry_row, const T* __restrict__ carry_val,
                                   T* __restrict__ y, int64_t n) {
@@ -329,6 +481,26 @@ int run_spmv(int kid, const Args& a) {
                 (long long)TB, (long long)W, (long long)TPT);
   const int threads = (int)(TB / TPT);
   const int64_t ncta = nnz == 0 ? 1 : ceil_div(nnz, TB);
+  if (a.params[5] == 0) {
+    // default: the schedule's Atomics strategy (zeroed y, red.add of partials)
+    if (int e = check_cuda(cudaMemsetAsync(y, 0, (size_t)M * sizeof(T), a.stream), "memset")) return e;
+    if (nnz == 0) return SPX_OK;
+    const int64_t nslots = ncta * (TB / W);
+    const size_t need = (size_t)(nslots + 1) * sizeof(int32_t);
+    if (!a.ws || a.ws_bytes < need) return fail(SPX_E_WORKSPACE, "workspace %zu < %zu bytes", a.ws_bytes, need);
+    int32_t* first = static_cast<int32_t*>(a.ws);
+    if (int e = launch_chunk_segments(pos, M, W, nslots, first, a.stream)) return e;
+    const unsigned g = (unsigned)ncta;
+    switch (TPT) {
+      case 4: spmv_nnz_atomic_kernel<T, 4><<<g, threads, 0, a.stream>>>(pos, crd, vals, x, y, M, nnz, W, 4, first); break;
+      case 8: spmv_nnz_atomic_kernel<T, 8><<<g, threads, 0, a.stream>>>(pos, crd, vals, x, y, M, nnz, W, 8, first); break;
+      case 16: spmv_nnz_atomic_kernel<T, 16><<<g, threads, 0, a.stream>>>(pos, crd, vals, x, y, M, nnz, W, 16, first); break;
+      default:
+        spmv_nnz_atomic_kernel<T, 0><<<g, threads, 0, a.stream>>>(pos, crd, vals, x, y, M, nnz, W, (int)TPT, first);
+    }
+    count_launch();
+    return check_cuda(cudaGetLastError(), "spmv_nnz_atomic_kernel");
+  }
   const NnzWorkspace L = nnz_workspace(ncta, sizeof(T));
   if (!a.ws || a.ws_bytes < L.total) return fail(SPX_E_WORKSPACE, "workspace %zu < %zu bytes", a.ws_bytes, L.total);
   T* carry_val = reinterpret_cast<T*>(static_cast<char*>(a.ws) + L.carry_val);
@@ -359,9 +531,12 @@ size_t ws_spmv(int kid, const Args& a) {
   if (kid != SPX_K_SPMV_NNZ) return 0;
   const int64_t nnz = a.level_sizes[1];
   const int64_t TB = a.params[0] > 0 ? a.params[0] : 1;
+  const int64_t W = a.params[1] > 0 ? a.params[1] : TB;
   const int64_t ncta = nnz == 0 ? 1 : ceil_div(nnz, TB);
   const size_t es = a.dtype == SPX_F32 ? 4 : 8;
-  return nnz_workspace(ncta, es).total;
+  const size_t atomic_ws = (size_t)(ncta * (TB / W > 0 ? TB / W : 1) + 1) * sizeof(int32_t);
+  const size_t det_ws = nnz_workspace(ncta, es).total;
+  return atomic_ws > det_ws ? atomic_ws : det_ws;
 }
 
 int launch_spmv(int kid, const Args& a) {

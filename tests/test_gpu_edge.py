@@ -99,7 +99,8 @@ def test_spmm_nnz_edges_f64(cuda, name, N, ring):
 @pytest.mark.parametrize("name", list(MATS))
 @pytest.mark.parametrize("TB,W,T", [(256, 256, 8), (128, 32, 1), (1024, 128, 4), (2048, 512, 16), (96, 96, 3)])
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
-def test_spmv_nnz_edges(cuda, name, TB, W, T, dtype):
+@pytest.mark.parametrize("strategy", [0, 1])  # params[5]: 0 atomics (default), 1 deterministic carry fix-up
+def test_spmv_nnz_edges(cuda, name, TB, W, T, dtype, strategy):
     pos, crd, vals, K = MATS[name]
     M = len(pos) - 1
     x = np.random.default_rng(3).uniform(-1, 1, K).astype(dtype)
@@ -109,7 +110,9 @@ def test_spmv_nnz_edges(cuda, name, TB, W, T, dtype):
     ops = {"A": DeviceTensor.from_arrays((M, K), "ds", {1: pos}, {1: crd}, v, device=cuda, dtype=dt),
            "x": DeviceTensor.dense(x, device=cuda, dtype=dt)}
     out = torch.full((M,), float("nan"), dtype=torch.float32 if dt == "f32" else torch.float64, device=cuda)
-    Executor(prog, ops, out, dtype=dt).launch()
+    ex = Executor(prog, ops, out, dtype=dt)
+    ex.plan.params[5] = strategy
+    ex.launch()
     got = out.cpu().numpy()
     assert not np.isnan(got).any()
     assert rel_err(got, O.spmv(pos, crd, v, x)) <= (1e-12 if dt == "f64" else 1e-5)
