@@ -161,6 +161,49 @@ int spx_partition_device(const int32_t* seg_start, int64_t nseg, int64_t nnz,
  * their place (DEVICE uint64_t[4]).  Parity tests require them equal. */
 int spx_selftest(uint64_t* out4, void* stream);
 
+/*
+ * Device-side pack: COO on the device -> the
+ * reference's coordinate hierarchy, bit-exact with spindle.tensors.pack
+ * (tensors.py:212-258) including CooTensor.normalized's duplicate folding
+ * (tensors.py:83-90).  The reference has no FFI for pack; these replace the
+ * body of `pack` for device-resident inputs and are driven phase by phase
+ * by formats.pack_device(), which allocates every output between phases
+ * from the counts the previous phase reports.
+ *
+ * spx_pack_sort: coords_host = host table of `order` DEVICE int32 arrays of
+ *   n coordinates; dims = host int64[order]; vals = DEVICE fp64[n].  Writes
+ *   ucoords (DEVICE int32[order][n], level-major, first nu entries of each
+ *   row used) and uvals (DEVICE fp64[n]) for the nu sorted unique entries,
+ *   and info (DEVICE int64[2]) = {nu, first out-of-bounds input index or -1}.
+ *   Workspace: spx_pack_workspace_size(n, order) bytes.
+ * spx_pack_level: one level of the hierarchy over the nu unique entries.
+ *   diff (DEVICE int64[nu], zero before level 0) accumulates the
+ *   prefix-change flags; slot (DEVICE int64[nu], zero before level 0) holds
+ *   the parent slots on entry and this level's slots on exit.  Dense levels
+ *   finish here; compressed levels also write the exclusive scan of diff
+ *   into ex and the level's stored count into *count_out (DEVICE int64),
+ *   then spx_pack_level_fill writes crd (count entries), pos
+ *   (parent_count + 1 entries) and moves slot to this level.
+ * spx_pack_vals: vals_out[slot[i]] = uvals[i] (the caller zero-fills
+ *   vals_out; dtype SPX_F64 or SPX_F32).
+ */
+size_t spx_pack_workspace_size(int64_t n, int32_t order);
+int spx_pack_sort(const int32_t* const* coords_host, int32_t order,
+                  const int64_t* dims, int64_t n, const double* vals,
+                  void* ws, size_t ws_bytes, int32_t* ucoords, double* uvals,
+                  int64_t* info, void* stream);
+size_t spx_pack_level_workspace_size(int64_t nu);
+int spx_pack_level(const int32_t* ucoord, int64_t nu, int32_t compressed,
+                   int64_t dim, int64_t parent_count, int64_t* diff,
+                   int64_t* slot, int64_t* ex, void* ws, size_t ws_bytes,
+                   int64_t* count_out, void* stream);
+int spx_pack_level_fill(const int32_t* ucoord, int64_t nu,
+                        const int64_t* diff, const int64_t* ex, int64_t* slot,
+                        int64_t count, int64_t parent_count, int32_t* crd_out,
+                        int32_t* pos_out, int64_t* cpar, void* stream);
+int spx_pack_vals(const int64_t* slot, const double* uvals, int64_t nu,
+                  void* vals_out, int32_t dtype, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

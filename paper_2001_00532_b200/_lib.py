@@ -61,6 +61,12 @@ EXPORTS = (
     "spx_partition",
     "spx_partition_device",
     "spx_selftest",
+    "spx_pack_workspace_size",
+    "spx_pack_sort",
+    "spx_pack_level_workspace_size",
+    "spx_pack_level",
+    "spx_pack_level_fill",
+    "spx_pack_vals",
 )
 
 
@@ -118,6 +124,19 @@ def load(path: str | os.PathLike | None = None):
     lib.spx_partition_device.restype = ctypes.c_int
     lib.spx_selftest.argtypes = [vp, vp]
     lib.spx_selftest.restype = ctypes.c_int
+    i64, sz = ctypes.c_int64, ctypes.c_size_t
+    lib.spx_pack_workspace_size.argtypes = [i64, ctypes.c_int32]
+    lib.spx_pack_workspace_size.restype = sz
+    lib.spx_pack_sort.argtypes = [ctypes.POINTER(vp), ctypes.c_int32, i64p, i64, vp, vp, sz, vp, vp, vp, vp]
+    lib.spx_pack_sort.restype = ctypes.c_int
+    lib.spx_pack_level_workspace_size.argtypes = [i64]
+    lib.spx_pack_level_workspace_size.restype = sz
+    lib.spx_pack_level.argtypes = [vp, i64, ctypes.c_int32, i64, i64, vp, vp, vp, vp, sz, vp, vp]
+    lib.spx_pack_level.restype = ctypes.c_int
+    lib.spx_pack_level_fill.argtypes = [vp, i64, vp, vp, vp, i64, i64, vp, vp, vp, vp]
+    lib.spx_pack_level_fill.restype = ctypes.c_int
+    lib.spx_pack_vals.argtypes = [vp, vp, i64, vp, ctypes.c_int32, vp]
+    lib.spx_pack_vals.restype = ctypes.c_int
     if path is None:
         _lib = lib
     return lib

@@ -1,0 +1,458 @@
+// Device-side pack: COO -> the reference's coordinate hierarchy on the GPU
+// (SURVEY.md §8(f) row 1), bit-exact with spindle.tensors.pack
+// (tensors.py:212-258) and CooTensor.normalized (tensors.py:83-90):
+//
+//   1. keys:    linearised coordinate key = ((c0*d1 + c1)*d2 + c2)...,
+//               bounds check (validate, tensors.py:75-81), idx = input order
+//   2. sort:    stable LSD radix sort of (key, idx) -- equal keys keep their
+//               input order, so duplicates fold left to right as the dict in
+//               normalized() does
+//   3. unique:  run starts; each run's values summed sequentially from +0.0
+//               in input order (`merged.get(c, 0.0) + value`)
+//   4. levels:  per level, the prefix-change flag of the sorted unique
+//               entries; Dense: slot = parent*dim + c; Compressed: slot =
+//               running count of first entries, crd = c at first entries,
+//               pos[p] = #first entries whose parent < p (the add.at/cumsum
+//               of tensors.py:241-243)
+//   5. vals:    zeros(parent_count) with the folded values at the leaf slots
+//
+// Every array is caller-allocated (the Python host in formats.py sizes them
+// between phases from the counts this file reports); nothing here allocates.
+#include <cmath>
+#include <utility>
+
+#include "spx_common.cuh"
+
+namespace spx {
+namespace {
+
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;  // 2048
+
+// ---------------------------------------------------------------------------
+// Exclusive scan of int64 (recursive over tile sums).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int64_t block_exclusive_scan(int64_t v, int64_t* s_warp, int64_t& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int64_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(kFull, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_warp[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = blockDim.x >> 5;
+    int64_t w = lane < nw ? s_warp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(kFull, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < nw) s_warp[lane] = w;
+  }
+  __syncthreads();
+  total = s_warp[(blockDim.x >> 5) - 1];
+  const int64_t before = warp > 0 ? s_warp[warp - 1] : 0;
+  __syncthreads();
+  return before + x - v;
+}
+
+__global__ void __launch_bounds__(kScanThreads) scan_tiles_kernel(const int64_t* __restrict__ in,
+                                                                  int64_t* __restrict__ out, int64_t n,
+                                                                  int64_t* __restrict__ tile_sums) {
+  __shared__ int64_t s_warp[32];
+  const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  int64_t v[kScanItems];
+  int64_t t = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    v[k] = base + k < n ? in[base + k] : 0;
+    t += v[k];
+  }
+  int64_t total;
+  int64_t run = block_exclusive_scan(t, s_warp, total);
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    if (base + k < n) out[base + k] = run;
+    run += v[k];
+  }
+  if (threadIdx.x == 0 && tile_sums) tile_sums[blockIdx.x] = total;
+}
+
+__global__ void add_tile_offsets_kernel(int64_t* __restrict__ out, int64_t n, const int64_t* __restrict__ offs) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] += offs[i / kScanTile];
+}
+
+size_t scan_ws_bytes(int64_t n) {
+  size_t b = 0;
+  while (n > kScanTile) {
+    n = ceil_div(n, kScanTile);
+    b += (size_t)n * 2 * sizeof(int64_t);
+  }
+  return b + 256;
+}
+
+// out[i] = sum(in[0..i)) ; returns SPX status.  ws holds the recursion.
+int exclusive_scan(const int64_t* in, int64_t* out, int64_t n, int64_t* ws, cudaStream_t s) {
+  if (n <= 0) return SPX_OK;
+  const int64_t tiles = ceil_div(n, kScanTile);
+  if (tiles == 1) {
+    scan_tiles_kernel<<<1, kScanThreads, 0, s>>>(in, out, n, nullptr);
+    count_launch();
+    return check_cuda(cudaGetLastError(), "scan_tiles_kernel");
+  }
+  int64_t* sums = ws;
+  int64_t* sums_scanned = ws + tiles;
+  scan_tiles_kernel<<<(unsigned)tiles, kScanThreads, 0, s>>>(in, out, n, sums);
+  count_launch();
+  if (int e = check_cuda(cudaGetLastError(), "scan_tiles_kernel")) return e;
+  if (int e = exclusive_scan(sums, sums_scanned, tiles, ws + 2 * tiles, s)) return e;
+  add_tile_offsets_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(out, n, sums_scanned);
+  count_launch();
+  return check_cuda(cudaGetLastError(), "add_tile_offsets_kernel");
+}
+
+// ---------------------------------------------------------------------------
+// Stable LSD radix sort of (uint64 key, uint32 idx), 8-bit digits.
+// ---------------------------------------------------------------------------
+constexpr int kSortThreads = 256;
+constexpr int kSortRounds = 16;
+constexpr int kSortTile = kSortThreads * kSortRounds;  // 4096 keys per tile
+
+__global__ void __launch_bounds__(kSortThreads) radix_hist_kernel(const uint64_t* __restrict__ keys, int64_t n,
+                                                                  int shift, int64_t ntiles,
+                                                                  int64_t* __restrict__ hist) {
+  __shared__ int s_hist[256];
+  s_hist[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * kSortTile;
+#pragma unroll 4
+  for (int r = 0; r < kSortRounds; ++r) {
+    const int64_t i = base + (int64_t)r * kSortThreads + threadIdx.x;
+    if (i < n) atomicAdd(&s_hist[(int)((keys[i] >> shift) & 0xff)], 1);
+  }
+  __syncthreads();
+  hist[(int64_t)threadIdx.x * ntiles + blockIdx.x] = s_hist[threadIdx.x];  // digit-major
+}
+
+// Stable scatter: element order inside a tile is round-major, then warp,
+// then lane; ranks come from __match_any_sync within a warp and per-round
+// per-warp digit counts in shared memory.
+__global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
+    const uint64_t* __restrict__ keys, const uint32_t* __restrict__ idx, int64_t n, int shift, int64_t ntiles,
+    const int64_t* __restrict__ offs, uint64_t* __restrict__ keys_out, uint32_t* __restrict__ idx_out) {
+  constexpr int NW = kSortThreads / 32;
+  __shared__ int s_cnt[NW][256];
+  __shared__ int64_t s_base[256];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int d_mine = threadIdx.x;  // the digit this thread keeps the running base of
+  int64_t run = offs[(int64_t)d_mine * ntiles + blockIdx.x];
+  const int64_t base = (int64_t)blockIdx.x * kSortTile;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int r = 0; r < kSortRounds; ++r) {
+    const int64_t i = base + (int64_t)r * kSortThreads + threadIdx.x;
+    const bool ok = i < n;
+    const uint64_t k = ok ? keys[i] : 0;
+    const uint32_t v = ok ? idx[i] : 0;
+    const int d = ok ? (int)((k >> shift) & 0xff) : 256;  // 256: no digit
+#pragma unroll
+    for (int w = 0; w < NW; ++w) s_cnt[w][threadIdx.x] = 0;
+    s_base[d_mine] = run;
+    __syncthreads();
+    const unsigned peers = __match_any_sync(kFull, d);
+    const int rank = __popc(peers & lt);
+    if (ok && rank == 0) s_cnt[warp][d] = __popc(peers);
+    __syncthreads();
+    // exclusive prefix over warps for digit d_mine
+    int acc = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      const int c = s_cnt[w][d_mine];
+      s_cnt[w][d_mine] = acc;
+      acc += c;
+    }
+    run += acc;
+    __syncthreads();
+    if (ok) {
+      const int64_t dst = s_base[d] + s_cnt[warp][d] + rank;
+      keys_out[dst] = k;
+      idx_out[dst] = v;
+    }
+    __syncthreads();
+  }
+}
+
+// Workspace carve-up of spx_pack_sort (one definition for sizing and use).
+struct PackLayout {
+  size_t dcoords, keys, idx, keys2, idx2, flags, ex, hist, offs, scan, total;
+};
+PackLayout pack_layout(int64_t n) {
+  PackLayout L;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t at = off;
+    off += (bytes + 255) & ~(size_t)255;
+    return at;
+  };
+  const size_t nn = (size_t)(n > 0 ? n : 1);
+  const int64_t ntiles = ceil_div(n > 0 ? n : 1, kSortTile);
+  L.dcoords = take(8 * sizeof(void*));
+  L.keys = take(nn * 8);
+  L.idx = take(nn * 4);
+  L.keys2 = take(nn * 8);
+  L.idx2 = take(nn * 4);
+  L.flags = take(nn * 8);
+  L.ex = take(nn * 8);
+  L.hist = take((size_t)256 * ntiles * 8);
+  L.offs = take((size_t)256 * ntiles * 8);
+  L.scan = take(scan_ws_bytes((int64_t)nn > 256 * ntiles ? (int64_t)nn : 256 * ntiles));
+  L.total = off;
+  return L;
+}
+
+// ---------------------------------------------------------------------------
+// pack phases
+// ---------------------------------------------------------------------------
+struct DimsArg {
+  int64_t d[8];
+  int order;
+};
+
+__global__ void pack_keys_kernel(DimsArg dims, const int32_t* const* __restrict__ coords, int64_t n,
+                                 uint64_t* __restrict__ keys, uint32_t* __restrict__ idx,
+                                 unsigned long long* __restrict__ first_bad) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint64_t k = 0;
+  bool bad = false;
+  for (int l = 0; l < dims.order; ++l) {
+    const int64_t c = coords[l][i];
+    bad |= c < 0 || c >= dims.d[l];
+    k = k * (uint64_t)dims.d[l] + (uint64_t)c;
+  }
+  keys[i] = k;
+  idx[i] = (uint32_t)i;
+  if (bad) atomicMin(first_bad, (unsigned long long)i);
+}
+
+// flags[i] = 1 at the first entry of each equal-key run
+__global__ void run_flags_kernel(const uint64_t* __restrict__ keys, int64_t n, int64_t* __restrict__ flags) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) flags[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1 : 0;
+}
+
+// run starts: fold the run's values in input order from +0.0 and emit the
+// unique entry's per-level coordinates (original input coordinates of the
+// run's first element)
+__global__ void unique_fold_kernel(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ idx,
+                                   const int64_t* __restrict__ flags, const int64_t* __restrict__ ex, int64_t n,
+                                   const double* __restrict__ vals, int order,
+                                   const int32_t* const* __restrict__ coords, int32_t* __restrict__ ucoords,
+                                   double* __restrict__ uvals, int64_t* __restrict__ nuniq) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (i == n - 1) *nuniq = ex[i] + flags[i];
+  if (!flags[i]) return;
+  const int64_t u = ex[i];
+  double acc = 0.0;
+  int64_t j = i;
+  do {
+    acc = acc + vals[idx[j]];
+    ++j;
+  } while (j < n && keys[j] == keys[i]);
+  uvals[u] = acc;
+  const uint32_t src = idx[i];
+  for (int l = 0; l < order; ++l) ucoords[(int64_t)l * n + u] = coords[l][src];
+}
+
+// prefix-change flags for level L: diff |= (c_L[i] != c_L[i-1]); diff[0] = 1
+__global__ void level_flags_kernel(const int32_t* __restrict__ c, int64_t n, int64_t* __restrict__ diff) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (i == 0) diff[0] = 1;
+  else if (c[i] != c[i - 1]) diff[i] = 1;
+}
+
+__global__ void dense_slot_kernel(const int32_t* __restrict__ c, int64_t n, int64_t dim, int64_t* __restrict__ slot) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) slot[i] = slot[i] * dim + c[i];
+}
+
+// compressed level: ex = exclusive scan of diff.  slot_new = ex + diff - 1;
+// first entries write crd and the compacted parent
+__global__ void compressed_fill_kernel(const int32_t* __restrict__ c, const int64_t* __restrict__ diff,
+                                       const int64_t* __restrict__ ex, int64_t n, int64_t* __restrict__ slot,
+                                       int32_t* __restrict__ crd_out, int64_t* __restrict__ cpar) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t k = ex[i] + diff[i] - 1;
+  if (diff[i]) {
+    crd_out[k] = c[i];
+    cpar[k] = slot[i];
+  }
+  slot[i] = k;
+}
+
+// pos[p] = #{k : cpar[k] < p} for p in [0, parent_count]
+__global__ void pos_fill_kernel(const int64_t* __restrict__ cpar, int64_t count, int64_t parent_count,
+                                int32_t* __restrict__ pos) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p > parent_count) return;
+  int64_t lo = 0, hi = count;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (cpar[mid] < p) lo = mid + 1;
+    else hi = mid;
+  }
+  pos[p] = (int32_t)lo;
+}
+
+__global__ void count_kernel(const int64_t* __restrict__ ex, const int64_t* __restrict__ flags, int64_t n,
+                             int64_t* __restrict__ out) {
+  *out = ex[n - 1] + flags[n - 1];
+}
+
+__global__ void vals_scatter_kernel(const int64_t* __restrict__ slot, const double* __restrict__ uvals, int64_t n,
+                                    double* __restrict__ out_f64, float* __restrict__ out_f32) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (out_f64) out_f64[slot[i]] = uvals[i];
+  else out_f32[slot[i]] = (float)uvals[i];
+}
+
+unsigned blocks_for(int64_t n) { return (unsigned)ceil_div(n > 0 ? n : 1, 256); }
+
+}  // namespace
+}  // namespace spx
+
+using namespace spx;
+
+extern "C" {
+
+size_t spx_pack_workspace_size(int64_t n, int32_t order) {
+  if (n < 0 || order < 1 || order > 8) return 0;
+  return pack_layout(n).total;
+}
+
+int spx_pack_sort(const int32_t* const* coords_host, int32_t order, const int64_t* dims, int64_t n,
+                  const double* vals, void* ws, size_t ws_bytes, int32_t* ucoords, double* uvals, int64_t* info,
+                  void* stream) {
+  if (order < 1 || order > 8 || n < 0 || !dims || !info) return fail(SPX_E_ARG, "spx_pack_sort: bad arguments");
+  if (n > 0 && (!coords_host || !vals || !ucoords || !uvals)) return fail(SPX_E_ARG, "spx_pack_sort: null buffer");
+  if (n > (int64_t)UINT32_MAX) return fail(SPX_E_UNSUPPORTED, "spx_pack_sort: more than 2^32 entries");
+  if (ws_bytes < spx_pack_workspace_size(n, order) || !ws) return fail(SPX_E_WORKSPACE, "pack workspace too small");
+  DimsArg da;
+  da.order = order;
+  double logsize = 0.0;
+  for (int l = 0; l < order; ++l) {
+    if (dims[l] < 1) return fail(SPX_E_ARG, "spx_pack_sort: dimension %d is %lld", l, (long long)dims[l]);
+    da.d[l] = dims[l];
+    logsize += log2((double)dims[l]);
+  }
+  if (logsize > 63.0) return fail(SPX_E_UNSUPPORTED, "spx_pack_sort: coordinate space exceeds 2^63 keys");
+  int bits = 0;
+  {
+    uint64_t total = 1;
+    for (int l = 0; l < order; ++l) total *= (uint64_t)dims[l];
+    while (bits < 64 && (total - 1) >> bits) ++bits;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // info[0] = unique count, info[1] = first out-of-bounds input index (or -1)
+  if (int e = check_cuda(cudaMemsetAsync(info, 0xff, 2 * sizeof(int64_t), s), "memset")) return e;
+  if (n == 0) return check_cuda(cudaMemsetAsync(info, 0, sizeof(int64_t), s), "memset");
+
+  const PackLayout L = pack_layout(n);
+  char* w = static_cast<char*>(ws);
+  const int32_t** dcoords = reinterpret_cast<const int32_t**>(w + L.dcoords);
+  uint64_t* keys = reinterpret_cast<uint64_t*>(w + L.keys);
+  uint32_t* idx = reinterpret_cast<uint32_t*>(w + L.idx);
+  uint64_t* keys2 = reinterpret_cast<uint64_t*>(w + L.keys2);
+  uint32_t* idx2 = reinterpret_cast<uint32_t*>(w + L.idx2);
+  int64_t* flags = reinterpret_cast<int64_t*>(w + L.flags);
+  int64_t* ex = reinterpret_cast<int64_t*>(w + L.ex);
+  const int64_t ntiles = ceil_div(n, kSortTile);
+  int64_t* hist = reinterpret_cast<int64_t*>(w + L.hist);
+  int64_t* offs = reinterpret_cast<int64_t*>(w + L.offs);
+  int64_t* scan_ws = reinterpret_cast<int64_t*>(w + L.scan);
+  if (int e = check_cuda(cudaMemcpyAsync(dcoords, coords_host, order * sizeof(void*), cudaMemcpyHostToDevice, s),
+                         "cudaMemcpyAsync"))
+    return e;
+  pack_keys_kernel<<<blocks_for(n), 256, 0, s>>>(da, dcoords, n, keys, idx,
+                                                 reinterpret_cast<unsigned long long*>(info + 1));
+  count_launch();
+  if (int e = check_cuda(cudaGetLastError(), "pack_keys_kernel")) return e;
+  for (int shift = 0; shift < bits; shift += 8) {
+    radix_hist_kernel<<<(unsigned)ntiles, kSortThreads, 0, s>>>(keys, n, shift, ntiles, hist);
+    count_launch();
+    if (int e = check_cuda(cudaGetLastError(), "radix_hist_kernel")) return e;
+    if (int e = exclusive_scan(hist, offs, 256 * ntiles, scan_ws, s)) return e;
+    radix_scatter_kernel<<<(unsigned)ntiles, kSortThreads, 0, s>>>(keys, idx, n, shift, ntiles, offs, keys2, idx2);
+    count_launch();
+    if (int e = check_cuda(cudaGetLastError(), "radix_scatter_kernel")) return e;
+    std::swap(keys, keys2);
+    std::swap(idx, idx2);
+  }
+  run_flags_kernel<<<blocks_for(n), 256, 0, s>>>(keys, n, flags);
+  count_launch();
+  if (int e = exclusive_scan(flags, ex, n, scan_ws, s)) return e;
+  unique_fold_kernel<<<blocks_for(n), 256, 0, s>>>(keys, idx, flags, ex, n, vals, order, dcoords, ucoords, uvals,
+                                                   info);
+  count_launch();
+  return check_cuda(cudaGetLastError(), "unique_fold_kernel");
+}
+
+int spx_pack_level(const int32_t* ucoord, int64_t nu, int32_t compressed, int64_t dim, int64_t parent_count,
+                   int64_t* diff, int64_t* slot, int64_t* ex, void* ws, size_t ws_bytes, int64_t* count_out,
+                   void* stream) {
+  if (nu < 0 || (nu > 0 && (!ucoord || !diff || !slot))) return fail(SPX_E_ARG, "spx_pack_level: bad arguments");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (nu == 0) return count_out ? check_cuda(cudaMemsetAsync(count_out, 0, 8, s), "memset") : SPX_OK;
+  level_flags_kernel<<<blocks_for(nu), 256, 0, s>>>(ucoord, nu, diff);
+  count_launch();
+  if (int e = check_cuda(cudaGetLastError(), "level_flags_kernel")) return e;
+  if (!compressed) {
+    dense_slot_kernel<<<blocks_for(nu), 256, 0, s>>>(ucoord, nu, dim, slot);
+    count_launch();
+    return check_cuda(cudaGetLastError(), "dense_slot_kernel");
+  }
+  if (!ex || !count_out || ws_bytes < scan_ws_bytes(nu)) return fail(SPX_E_WORKSPACE, "pack level workspace");
+  if (int e = exclusive_scan(diff, ex, nu, static_cast<int64_t*>(ws), s)) return e;
+  count_kernel<<<1, 1, 0, s>>>(ex, diff, nu, count_out);
+  count_launch();
+  (void)parent_count;
+  return check_cuda(cudaGetLastError(), "count_kernel");
+}
+
+size_t spx_pack_level_workspace_size(int64_t nu) { return scan_ws_bytes(nu); }
+
+int spx_pack_level_fill(const int32_t* ucoord, int64_t nu, const int64_t* diff, const int64_t* ex, int64_t* slot,
+                        int64_t count, int64_t parent_count, int32_t* crd_out, int32_t* pos_out, int64_t* cpar,
+                        void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (!pos_out) return fail(SPX_E_ARG, "spx_pack_level_fill: null pos");
+  if (nu > 0) {
+    compressed_fill_kernel<<<blocks_for(nu), 256, 0, s>>>(ucoord, diff, ex, nu, slot, crd_out, cpar);
+    count_launch();
+    if (int e = check_cuda(cudaGetLastError(), "compressed_fill_kernel")) return e;
+  }
+  pos_fill_kernel<<<blocks_for(parent_count + 1), 256, 0, s>>>(cpar, nu > 0 ? count : 0, parent_count, pos_out);
+  count_launch();
+  return check_cuda(cudaGetLastError(), "pos_fill_kernel");
+}
+
+int spx_pack_vals(const int64_t* slot, const double* uvals, int64_t nu, void* vals_out, int32_t dtype,
+                  void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (nu == 0) return SPX_OK;
+  vals_scatter_kernel<<<blocks_for(nu), 256, 0, s>>>(slot, uvals, nu,
+                                                     dtype == SPX_F64 ? static_cast<double*>(vals_out) : nullptr,
+                                                     dtype == SPX_F32 ? static_cast<float*>(vals_out) : nullptr);
+  count_launch();
+  return check_cuda(cudaGetLastError(), "vals_scatter_kernel");
+}
+
+}  // extern "C"
