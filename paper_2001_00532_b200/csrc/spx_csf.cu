@@ -194,15 +194,16 @@ __device__ __forceinline__ void mttkrp_walk(const MttkrpCtx<T, VPL, CONTIG>& c, 
   // this lane's slice of D: row l starts at Dl + l*R (32-bit offsets)
   const char* __restrict__ Dl = reinterpret_cast<const char*>(c.Dm + (CONTIG ? lane * VPL : lane));
   const uint32_t rowb = (uint32_t)(c.R * (int64_t)sizeof(T));
-  auto drow = [&](Fr& d, int l) {
-    const T* src = reinterpret_cast<const T*>(addr_wide(Dl, (uint32_t)l, rowb));
-    if constexpr (CONTIG) {
-      d.load_ptr(src);
-    } else {
-#pragma unroll
-      for (int i = 0; i < VPL; ++i) d.v[i] = (i * 32 + lane < ncols) ? __ldg(src + i * 32) : T(0);
-    }
-  };
+#define SPX_DROW(d, l)                                                                       \
+  do {                                                                                       \
+    const T* src_ = reinterpret_cast<const T*>(addr_wide(Dl, (uint32_t)(l), rowb));         \
+    if constexpr (CONTIG) {                                                                  \
+      (d).load_ptr(src_);                                                                    \
+    } else {                                                                                 \
+      _Pragma("unroll") for (int i_ = 0; i_ < VPL; ++i_)(d).v[i_] =                         \
+          (i_ * 32 + lane < ncols) ? __ldg(src_ + i_ * 32) : T(0);                          \
+    }                                                                                        \
+  } while (0)
   LeafRing<T, kLeafRing> ring;
   ring.init(ring_base, c.crd2, c.vals, q0, q1);
   ring.prologue(lane, pol_s);
@@ -212,30 +213,31 @@ __device__ __forceinline__ void mttkrp_walk(const MttkrpCtx<T, VPL, CONTIG>& c, 
     const int n = min(32, q1 - p);
     const int32_t* Ls = ring.crd_slot(b);
     const T* Vs = ring.val_slot(b);
-    // aligned groups of four leaves: one 16 B broadcast of coordinates, four
-    // row reads of D; a group that crosses a fiber end takes the slow path
-#pragma unroll 2
-    for (int t = 0; t < n; t += 4) {
-      const int4 l4 = *reinterpret_cast<const int4*>(Ls + t);  // zero-filled past n
-      Fr d0, d1, d2, d3;
-      drow(d0, l4.x);
-      drow(d1, l4.y);
-      drow(d2, l4.z);
-      drow(d3, l4.w);
-      if (p + t + 4 <= fend && t + 4 <= n) {
-        accf.fma(Vs[t], d0);
-        accf.fma(Vs[t + 1], d1);
-        accf.fma(Vs[t + 2], d2);
-        accf.fma(Vs[t + 3], d3);
-      } else {
-        const Fr* dd[4] = {&d0, &d1, &d2, &d3};
+    // groups of G leaves: all G row reads of D are issued before the first
+    // FMA (G*VPL = 16 values per lane in flight), then the group is consumed
+    // fiber segment by fiber segment (predicated FMAs keep d[] in registers)
+    constexpr int G = (16 / VPL) < 4 ? 4 : (16 / VPL);
+#pragma unroll 1
+    for (int t = 0; t < n; t += G) {
+      Fr d[G];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (t + u < n) {
-            if (p + t + u >= fend) advance_to(p + t + u);
-            accf.fma(Vs[t + u], *dd[u]);
-          }
-        }
+      for (int u = 0; u < G; u += 4) {
+        const int4 l4 = *reinterpret_cast<const int4*>(Ls + t + u);  // zero-filled past n
+        SPX_DROW(d[u], l4.x);
+        SPX_DROW(d[u + 1], l4.y);
+        SPX_DROW(d[u + 2], l4.z);
+        SPX_DROW(d[u + 3], l4.w);
+      }
+      const int cnt = min(G, n - t);
+      int u0 = 0;
+      while (true) {
+        const int u1 = min(cnt, fend - (p + t));  // leaves [u0, u1) lie in fiber f
+#pragma unroll
+        for (int u = 0; u < G; ++u)
+          if (u >= u0 && u < u1) accf.fma(Vs[t + u], d[u]);
+        if (u1 >= cnt) break;
+        u0 = u1;
+        advance_to(p + t + u0);
       }
     }
     ring.release();
@@ -244,6 +246,7 @@ __device__ __forceinline__ void mttkrp_walk(const MttkrpCtx<T, VPL, CONTIG>& c, 
   for (int i = 0; i < VPL; ++i) accs.v[i] += accf.v[i] * crow.v[i];
   flush_slice();
 }
+#undef SPX_DROW
 
 constexpr int kMttkrpThreads = 512;
 constexpr size_t kSmemBudget = 200 * 1024;
