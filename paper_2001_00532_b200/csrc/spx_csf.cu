@@ -214,9 +214,9 @@ __device__ __forceinline__ void mttkrp_walk(const MttkrpCtx<T, VPL, CONTIG>& c, 
     const int32_t* Ls = ring.crd_slot(b);
     const T* Vs = ring.val_slot(b);
     // groups of G leaves: all G row reads of D are issued before the first
-    // FMA (G*VPL = 16 values per lane in flight), then the group is consumed
+    // FMA (G*VPL >= 8 values per lane in flight), then the group is consumed
     // fiber segment by fiber segment (predicated FMAs keep d[] in registers)
-    constexpr int G = (16 / VPL) < 4 ? 4 : (16 / VPL);
+    constexpr int G = (8 / VPL) < 4 ? 4 : (8 / VPL);
 #pragma unroll 1
     for (int t = 0; t < n; t += G) {
       Fr d[G];
@@ -228,16 +228,25 @@ __device__ __forceinline__ void mttkrp_walk(const MttkrpCtx<T, VPL, CONTIG>& c, 
         SPX_DROW(d[u + 2], l4.z);
         SPX_DROW(d[u + 3], l4.w);
       }
-      const int cnt = min(G, n - t);
-      int u0 = 0;
-      while (true) {
-        const int u1 = min(cnt, fend - (p + t));  // leaves [u0, u1) lie in fiber f
+      T vg[G];
 #pragma unroll
-        for (int u = 0; u < G; ++u)
-          if (u >= u0 && u < u1) accf.fma(Vs[t + u], d[u]);
-        if (u1 >= cnt) break;
-        u0 = u1;
-        advance_to(p + t + u0);
+      for (int u = 0; u < G; ++u) vg[u] = Vs[t + u];  // zero-filled past n
+      const int cnt = min(G, n - t);
+      if (cnt == G && p + t + G <= fend) {
+        // the whole group lies in fiber f
+#pragma unroll
+        for (int u = 0; u < G; ++u) accf.fma(vg[u], d[u]);
+      } else {
+        int u0 = 0;
+        while (true) {
+          const int u1 = min(cnt, fend - (p + t));  // leaves [u0, u1) lie in fiber f
+#pragma unroll
+          for (int u = 0; u < G; ++u)
+            if (u >= u0 && u < u1) accf.fma(vg[u], d[u]);
+          if (u1 >= cnt) break;
+          u0 = u1;
+          advance_to(p + t + u0);
+        }
       }
     }
     ring.release();
