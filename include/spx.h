@@ -187,6 +187,24 @@ int spx_selftest(uint64_t* out4, void* stream);
  * spx_pack_vals: vals_out[slot[i]] = uvals[i] (the caller zero-fills
  *   vals_out; dtype SPX_F64 or SPX_F32).
  */
+/*
+ * Native tensor-file ingest, host-side, for
+ * spindle.fileio's formats (fileio.py:66-162): fmt 0 = Matrix Market,
+ * 1 = FROSTT.  spx_text_scan reports order, entry count and dims (FROSTT:
+ * the last '# dims:' comment, or -1 = infer); spx_text_parse writes 0-based
+ * int32 coordinates (level-major, coords[l*n + i]) and fp64 values in file
+ * order into HOST buffers and fills inferred FROSTT dims.  Both return
+ * SPX_PARSE_DEFER for any file they do not accept verbatim (malformed or
+ * out-of-bounds entries, count mismatches, non-ASCII, Python-only literal
+ * syntax); the host then runs the reference parser, which raises the exact
+ * error (or accepts the literal).
+ */
+#define SPX_PARSE_DEFER 1
+int spx_text_scan(const char* text, int64_t len, int32_t fmt, int32_t* order_out,
+                  int64_t* n_out, int64_t* dims_out);
+int spx_text_parse(const char* text, int64_t len, int32_t fmt, int32_t order,
+                   int64_t n, int64_t* dims, int32_t* coords, double* vals);
+
 size_t spx_pack_workspace_size(int64_t n, int32_t order);
 int spx_pack_sort(const int32_t* const* coords_host, int32_t order,
                   const int64_t* dims, int64_t n, const double* vals,

@@ -67,6 +67,8 @@ EXPORTS = (
     "spx_pack_level",
     "spx_pack_level_fill",
     "spx_pack_vals",
+    "spx_text_scan",
+    "spx_text_parse",
 )
 
 
@@ -137,6 +139,10 @@ def load(path: str | os.PathLike | None = None):
     lib.spx_pack_level_fill.restype = ctypes.c_int
     lib.spx_pack_vals.argtypes = [vp, vp, i64, vp, ctypes.c_int32, vp]
     lib.spx_pack_vals.restype = ctypes.c_int
+    lib.spx_text_scan.argtypes = [ctypes.c_char_p, i64, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32), i64p, i64p]
+    lib.spx_text_scan.restype = ctypes.c_int
+    lib.spx_text_parse.argtypes = [ctypes.c_char_p, i64, ctypes.c_int32, ctypes.c_int32, i64, i64p, vp, vp]
+    lib.spx_text_parse.restype = ctypes.c_int
     if path is None:
         _lib = lib
     return lib

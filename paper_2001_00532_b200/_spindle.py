@@ -52,6 +52,6 @@ def available() -> bool:
 
 ensure_ok = available()
 if ensure_ok:
-    from spindle import errors, graph, ir, notation, schedule, tensors  # noqa: E402,F401
+    from spindle import errors, fileio, graph, ir, notation, schedule, tensors  # noqa: E402,F401
 else:  # pragma: no cover - exercised only without the reference installed
-    errors = graph = ir = notation = schedule = tensors = None  # type: ignore[assignment]
+    errors = fileio = graph = ir = notation = schedule = tensors = None  # type: ignore[assignment]

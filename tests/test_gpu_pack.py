@@ -113,3 +113,22 @@ def test_pack_device_feeds_the_kernels(cuda):
                  T.parse_format("ds"))
     want = O.spmv(ref.pos[1], ref.crd[1], ref.vals, x)
     assert np.max(np.abs(y.data - want)) <= 1e-12
+
+
+def test_read_tensor_device_matches_reference(cuda, tmp_path):
+    from paper_2001_00532_b200.fileio import read_tensor_device
+
+    rng = np.random.default_rng(11)
+    n = 5000
+    i, j = rng.integers(1, 301, n), rng.integers(1, 201, n)
+    lines = ["%%MatrixMarket matrix coordinate real general", f"300 200 {n}"]
+    lines += [f"{a} {b} {float(c)!r}" for a, b, c in zip(i, j, rng.uniform(-1, 1, n))]
+    mtx = tmp_path / "a.mtx"
+    mtx.write_text("\n".join(lines) + "\n")
+    tns = tmp_path / "b.tns"
+    k = rng.integers(1, 9, (n, 3))
+    tns.write_text("\n".join(" ".join(map(str, r)) + f" {float(v)!r}" for r, v in zip(k, rng.uniform(-1, 1, n))))
+    for path, levels in ((mtx, "ds"), (mtx, "ss"), (tns, "sss"), (tns, "dss")):
+        want = T.pack(_spindle.fileio.read_tensor_file(path), T.parse_format(levels))
+        got = read_tensor_device(path, levels, device=cuda)
+        _check(got, want.dims, levels, want.pos, want.crd, want.vals)
