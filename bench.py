@@ -286,7 +286,11 @@ def main():
             # what binds this kernel: every nonzero gathers one N-wide row of B
             # from L2; the L2->SM rate achieved on it
             "gathered_bytes_per_launch": int(nnz_local * N * 4),
-            "gather_TBs": round(nnz_local * N * 4 / (statistics.mean(times) * 1e-3) / 1e12, 2)}
+            "gather_TBs": round(nnz_local * N * 4 / (statistics.mean(times) * 1e-3) / 1e12, 2),
+            # the same rate against the measured ceiling of 512 B-row gathers on
+            # this part (18.9 TB/s: L2-resident rows, no arithmetic; tools/gbench2.py,
+            # profiles/r01_gather_paths.txt)
+            "gather_frac": round(nnz_local * N * 4 / (statistics.mean(times) * 1e-3) / 18.9e12, 3)}
 
     # gather of the sharded output (reported separately)
     gather_ms = None
