@@ -348,11 +348,18 @@ __global__ void carry_fixup_kernel(const int32_t* __restrict__ carry_row, const 
   s.add_into(C + col0 + (int64_t)row * N, lane, ncols);
 }
 
+// K5 warp-per-row: the row's (column, value) pairs stream through the
+// warp's cp.async LeafRing (three batches ahead) and come back as 16 B
+// broadcasts; B rows are gathered U at a time into registers.  A row longer
+// than the ring keeps streaming, so one warp on a long row still has ~U rows
+// of B and three batches of A in flight.
 template <typename T, int VPL, bool CONTIG, int U>
-__global__ void __launch_bounds__(kMaxThreads) spmm_row_kernel(
+__global__ void __launch_bounds__(kMaxThreads, 2) spmm_row_kernel(
     const int32_t* __restrict__ pos, const int32_t* __restrict__ crd, const T* __restrict__ vals,
     const T* __restrict__ B, T* __restrict__ C, int64_t M, int64_t N, int64_t R) {
   using F = Frag<T, VPL, CONTIG>;
+  using Ring = LeafRing<T, 4>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int PW = 32 * VPL;
   const int nw = blockDim.x >> 5;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -360,37 +367,42 @@ __global__ void __launch_bounds__(kMaxThreads) spmm_row_kernel(
   const int ncols = (int)min((int64_t)PW, N - col0);
   const T* __restrict__ Bp = B + col0;
   T* __restrict__ Cp = C + col0;
+  const uint64_t pol_s = l2_evict_first();
+  const char* __restrict__ Bl = reinterpret_cast<const char*>(Bp + (CONTIG ? lane * VPL : 0));
+  const uint32_t rowb = (uint32_t)(N * (int64_t)sizeof(T));
   const int64_t rows_lo = (int64_t)blockIdx.x * R;
-  const int64_t nwr = (R + nw - 1) / nw;
-  for (int64_t wr = 0; wr < nwr; ++wr) {
-    const int64_t br = wr * nw + warp;  // block_row = warp_row*WARPS + warp
+  const int nwr = (int)((R + nw - 1) / nw);
+  for (int wr = 0; wr < nwr; ++wr) {
+    const int64_t br = (int64_t)wr * nw + warp;  // block_row = warp_row*WARPS + warp
     if (br >= R) break;
     const int64_t row = rows_lo + br;
     if (row >= M) break;
-    const int64_t a = __ldg(pos + row), e = __ldg(pos + row + 1);
+    const int a = __ldg(pos + row), e = __ldg(pos + row + 1);
     F acc;
     acc.zero();
-    for (int64_t p = a; p < e; p += 32) {
-      const int n = (int)min((int64_t)32, e - p);
-      int my_c = 0;
-      T my_v = T(0);
-      if (lane < n) {
-        my_c = __ldcs(crd + p + lane);
-        my_v = __ldcs(vals + p + lane);
-      }
-      for (int t0 = 0; t0 < n; t0 += U) {
-        F b[U];
+    Ring ring;
+    ring.init(smem_raw + (size_t)warp * Ring::kBytes, crd, vals, a, e);
+    ring.prologue(lane, pol_s);
+    for (int b = 0; b < ring.nb; ++b) {
+      ring.acquire(b, lane, pol_s);
+      const int n = min(32, e - (a + b * 32));
+      const int32_t* Cs = ring.crd_slot(b);
+      const T* Vs = ring.val_slot(b);
+#pragma unroll 1
+      for (int t = 0; t < n; t += U) {
+        F bb[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const int c = __shfl_sync(kFull, my_c, (t0 + u) & 31);
-          if (t0 + u < n) b[u].load(Bp + (int64_t)c * N, lane, ncols);
+          const int c = Cs[t + u];  // zero-filled past n
+          const T* src = reinterpret_cast<const T*>(addr_wide(Bl, (uint32_t)c, rowb));
+          if constexpr (CONTIG) bb[u].load_ptr(src);
+          else bb[u].load(src, lane, ncols);
         }
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const T v = __shfl_sync(kFull, my_v, (t0 + u) & 31);
-          if (t0 + u < n) acc.fma(v, b[u]);
-        }
+        for (int u = 0; u < U; ++u)
+          if (t + u < n) acc.fma(Vs[t + u], bb[u]);
       }
+      ring.release();
     }
     acc.store(Cp + row * N, lane, ncols);
   }
@@ -515,7 +527,9 @@ int run_spmm(int kid, const Args& a, const SpmmGeom& g) {
   int64_t nw = a.params[1] > 0 ? a.params[1] : (R < 8 ? R : 8);
   if (nw > kMaxWarps) nw = kMaxWarps;
   dim3 grid((unsigned)ceil_div(M, R), (unsigned)g.npanels);
-  spmm_row_kernel<T, VPL, CONTIG, U><<<grid, (unsigned)(nw * 32), 0, a.stream>>>(pos, crd, vals, B, C, M, N, R);
+  constexpr int UR = U > 4 ? 4 : U;  // B rows in flight per warp (register budget)
+  spmm_row_kernel<T, VPL, CONTIG, UR><<<grid, (unsigned)(nw * 32), (size_t)nw * LeafRing<T, 4>::kBytes, a.stream>>>(
+      pos, crd, vals, B, C, M, N, R);
   count_launch();
   return check_cuda(cudaGetLastError(), "spmm_row_kernel");
 }

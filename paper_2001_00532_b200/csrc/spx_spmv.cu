@@ -25,7 +25,7 @@ namespace {
 constexpr int kPosCache = 4096;  // ints of pos staged per CTA
 
 template <typename T>
-__global__ void __launch_bounds__(kMaxThreads) spmv_row_kernel(const int32_t* __restrict__ pos,
+__global__ void __launch_bounds__(kMaxThreads, 2) spmv_row_kernel(const int32_t* __restrict__ pos,
                                                         const int32_t* __restrict__ crd,
                                                         const T* __restrict__ vals, const T* __restrict__ x,
                                                         T* __restrict__ y, int64_t M, int64_t R) {
@@ -33,15 +33,31 @@ __global__ void __launch_bounds__(kMaxThreads) spmv_row_kernel(const int32_t* __
   for (int64_t t = threadIdx.x; t < R; t += blockDim.x) {
     const int64_t i = lo + t;
     if (i >= M) return;
-    const int64_t a = __ldg(pos + i), e = __ldg(pos + i + 1);
+    const int a = __ldg(pos + i), e = __ldg(pos + i + 1);
+    // eight positions' loads in flight per step (a long row is one thread's
+    // serial dependency chain otherwise); sequential fold order kept
     T acc = T(0);
-    for (int64_t p = a; p < e; ++p) acc += __ldcs(vals + p) * __ldg(x + __ldcs(crd + p));
+    int p = a;
+    for (; p + 8 <= e; p += 8) {
+      int c[8];
+      T v[8], xv[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        c[k] = __ldcs(crd + p + k);
+        v[k] = __ldcs(vals + p + k);
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) xv[k] = __ldg(x + c[k]);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc += v[k] * xv[k];
+    }
+    for (; p < e; ++p) acc += __ldcs(vals + p) * __ldg(x + __ldcs(crd + p));
     __stcs(y + i, acc);
   }
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kMaxThreads) spmv_warp_kernel(const int32_t* __restrict__ pos,
+__global__ void __launch_bounds__(kMaxThreads, 2) spmv_warp_kernel(const int32_t* __restrict__ pos,
                                                          const int32_t* __restrict__ crd,
                                                          const T* __restrict__ vals, const T* __restrict__ x,
                                                          T* __restrict__ y, int64_t M, int64_t R) {
@@ -54,9 +70,25 @@ __global__ void __launch_bounds__(kMaxThreads) spmv_warp_kernel(const int32_t* _
     if (br >= R) break;
     const int64_t i = lo + br;
     if (i >= M) break;
-    const int64_t a = __ldg(pos + i), e = __ldg(pos + i + 1);
+    const int a = __ldg(pos + i), e = __ldg(pos + i + 1);
+    // lanes stride the row (thread_nz x thread); four 32-position steps'
+    // loads are in flight at once, then the Temporary fold
     T acc = T(0);
-    for (int64_t p = a + lane; p < e; p += 32) acc += __ldcs(vals + p) * __ldg(x + __ldcs(crd + p));
+    int p = a + lane;
+    for (; p + 96 < e; p += 128) {
+      int c[4];
+      T v[4], xv[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        c[k] = __ldcs(crd + p + 32 * k);
+        v[k] = __ldcs(vals + p + 32 * k);
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) xv[k] = __ldg(x + c[k]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) acc += v[k] * xv[k];
+    }
+    for (; p < e; p += 32) acc += __ldcs(vals + p) * __ldg(x + __ldcs(crd + p));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
     if (lane == 0) __stcs(y + i, acc);
