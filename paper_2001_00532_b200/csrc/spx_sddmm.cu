@@ -8,31 +8,16 @@
 //  K6 SPX_K_SDDMM_NNZ: fuse(i,j,f) pos(f,fpos,B) split(fpos,block,..,NNZ_PER_TB)
 //     split(..,warp,nnz,NNZ_PER_WARP) split(k,dvu,thread,32)
 //     bound(dvu,dense_val,ceil(K/32),MaxExact), thread:Temporary.
-//     A warp walks NNZ_PER_WARP positions; lanes cover k; the 32 dot products
-//     of a batch are reduced with a 31-shuffle transpose-reduction so lane t
-//     ends with nonzero t's value and the store is coalesced.  Each position
+//     A warp walks NNZ_PER_WARP positions; lanes cover k; each group of eight
+//     dot products is folded with an eight-wide transpose-reduction and lane t
+//     ends with nonzero t's value, so the store is coalesced.  Each position
 //     writes its own output: no races, no carries.
-//  K10 SPX_K_SDDMM_ROW: warp per row (row-split / unscheduled shapes).
+//  K10 SPX_K_SDDMM_ROW: warp per row (row-split / unscheduled shapes), the
+//     same batch pipeline one row at a time.
 #include "spx_common.cuh"
 
 namespace spx {
 namespace {
-
-// part[t] on every lane -> lane t returns sum over lanes of part[t]
-template <typename T>
-__device__ __forceinline__ T transpose_reduce(T (&part)[32], int lane) {
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) {
-    const bool upper = (lane & o) != 0;
-#pragma unroll
-    for (int i = 0; i < o; ++i) {
-      const T send = upper ? part[i] : part[i + o];
-      const T keep = upper ? part[i + o] : part[i];
-      part[i] = keep + __shfl_xor_sync(kFull, send, o);
-    }
-  }
-  return part[0];
-}
 
 template <typename T, int VPL, bool CONTIG>
 __device__ __forceinline__ T dot(const Frag<T, VPL, CONTIG>& a, const Frag<T, VPL, CONTIG>& b) {
@@ -47,57 +32,6 @@ __device__ __forceinline__ void emit(T* __restrict__ out, bool dense, int64_t N,
                                      T val) {
   if (dense) out[r * N + c] = val;
   else __stcs(out + p, val);
-}
-
-// one batch of up to 32 positions starting at p, all of them in rows tracked
-// by (r, rend).  ROWFIXED: the caller guarantees a single row.
-template <typename T, int VPL, bool CONTIG, int U, bool ROWFIXED>
-__device__ __forceinline__ void sddmm_batch(const int32_t* __restrict__ pos, const int32_t* __restrict__ crd,
-                                            const T* __restrict__ vals, const T* __restrict__ Cm,
-                                            const T* __restrict__ Dm, T* __restrict__ out, int64_t M, int64_t N,
-                                            int64_t K, bool dense, int64_t p, int n, int64_t& r, int64_t& rend,
-                                            RowEndCache& ends, Frag<T, VPL, CONTIG>& crow, int lane) {
-  using F = Frag<T, VPL, CONTIG>;
-  int my_c = 0;
-  T my_v = T(0);
-  if (lane < n) {
-    my_c = __ldcs(crd + p + lane);
-    my_v = __ldcs(vals + p + lane);
-  }
-  // row of my position (for the dense scatter)
-  int64_t my_r = r;
-  T part[32];
-#pragma unroll
-  for (int t0 = 0; t0 < 32; t0 += U) {
-    F d[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int c = __shfl_sync(kFull, my_c, t0 + u);
-      if (t0 + u < n) d[u].load(Dm + (int64_t)c * K, lane, (int)K);
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int t = t0 + u;
-      if (t < n) {
-        if (!ROWFIXED) {
-          const int64_t pp = p + t;
-          if (pp >= rend) {
-            while (pp >= rend) {
-              ++r;
-              rend = ends.end(pos, r, M, lane);
-            }
-            crow.load(Cm + r * K, lane, (int)K);
-          }
-          if (lane == t) my_r = r;
-        }
-        part[t] = dot(crow, d[u]);
-      } else {
-        part[t] = T(0);
-      }
-    }
-  }
-  const T s = transpose_reduce(part, lane);
-  if (lane < n) emit(out, dense, N, p + lane, my_r, my_c, my_v * s);
 }
 
 // part[i] (i < 8) on every lane -> lanes with (lane & 3) == 0 hold the sum
@@ -206,41 +140,76 @@ __global__ void __launch_bounds__(kMaxThreads, 2) sddmm_nnz_kernel(const int32_t
   }
 }
 
+// K10 warp-per-row: the same batch pipeline as K6 over one row at a time
+// (C row loaded once per row, (column, value) pairs on the warp's LeafRing,
+// eight dot products per transpose_reduce8, coalesced stores).
 template <typename T, int VPL, bool CONTIG, int U>
-__global__ void __launch_bounds__(kMaxThreads) sddmm_row_kernel(const int32_t* __restrict__ pos,
-                                                         const int32_t* __restrict__ crd,
-                                                         const T* __restrict__ vals, const T* __restrict__ Cm,
-                                                         const T* __restrict__ Dm, T* __restrict__ out, int64_t M,
-                                                         int64_t N, int64_t K, int64_t R, bool dense) {
+__global__ void __launch_bounds__(kMaxThreads, 2) sddmm_row_kernel(const int32_t* __restrict__ pos,
+                                                            const int32_t* __restrict__ crd,
+                                                            const T* __restrict__ vals, const T* __restrict__ Cm,
+                                                            const T* __restrict__ Dm, T* __restrict__ out, int64_t M,
+                                                            int64_t N, int64_t K, int64_t R, bool dense) {
+  using F = Frag<T, VPL, CONTIG>;
+  using Ring = LeafRing<T, 4>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   const int nw = blockDim.x >> 5;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ncols = (int)K;
+  const uint64_t pol_s = l2_evict_first();
+  const char* __restrict__ Dl = reinterpret_cast<const char*>(Dm + (CONTIG ? lane * VPL : lane));
+  const uint32_t rowb = (uint32_t)(K * (int64_t)sizeof(T));
   const int64_t lo = (int64_t)blockIdx.x * R;
-  const int64_t nwr = (R + nw - 1) / nw;
-  RowEndCache ends;  // unused on the fixed-row path
-  ends.base = 0;
-  ends.mine = 0;
-  for (int64_t wr = 0; wr < nwr; ++wr) {
-    const int64_t br = wr * nw + warp;
+  const int nwr = (int)((R + nw - 1) / nw);
+  for (int wr = 0; wr < nwr; ++wr) {
+    const int64_t br = (int64_t)wr * nw + warp;
     if (br >= R) break;
-    int64_t r = lo + br;
+    const int64_t r = lo + br;
     if (r >= M) break;
-    const int64_t a = __ldg(pos + r), e = __ldg(pos + r + 1);
+    const int a = __ldg(pos + r), e = __ldg(pos + r + 1);
     if (a == e) continue;
-    Frag<T, VPL, CONTIG> crow;
-    crow.load(Cm + r * K, lane, (int)K);
-    int64_t rend = e;
-    for (int64_t p = a; p < e; p += 32) {
-      const int n = (int)min((int64_t)32, e - p);
-      sddmm_batch<T, VPL, CONTIG, U, true>(pos, crd, vals, Cm, Dm, out, M, N, K, dense, p, n, r, rend, ends, crow,
-                                           lane);
+    F crow;
+    crow.load(Cm + r * K, lane, ncols);
+    Ring ring;
+    ring.init(smem_raw + (size_t)warp * Ring::kBytes, crd, vals, a, e);
+    ring.prologue(lane, pol_s);
+    for (int b = 0; b < ring.nb; ++b) {
+      ring.acquire(b, lane, pol_s);
+      const int p = a + b * 32;
+      const int n = min(32, e - p);
+      const int32_t* Cs = ring.crd_slot(b);
+      const T* Vs = ring.val_slot(b);
+      T res = T(0);
+#pragma unroll 1
+      for (int g = 0; g < 4 && g * 8 < n; ++g) {
+        T part[8];
+#pragma unroll
+        for (int u0 = 0; u0 < 8; u0 += U) {
+          F d[U];
+#pragma unroll
+          for (int uu = 0; uu < U; ++uu) {
+            const T* src = reinterpret_cast<const T*>(addr_wide(Dl, (uint32_t)Cs[g * 8 + u0 + uu], rowb));
+            if constexpr (CONTIG) {
+              d[uu].load_ptr(src);
+            } else {
+#pragma unroll
+              for (int i = 0; i < VPL; ++i) d[uu].v[i] = (i * 32 + lane < ncols) ? __ldg(src + i * 32) : T(0);
+            }
+          }
+#pragma unroll
+          for (int uu = 0; uu < U; ++uu) part[u0 + uu] = (g * 8 + u0 + uu < n) ? dot(crow, d[uu]) : T(0);
+        }
+        const T sum = transpose_reduce8(part, lane);
+        const T got = __shfl_sync(kFull, sum, (lane & 7) * 4);
+        if ((lane >> 3) == g) res = got;
+      }
+      if (lane < n) emit(out, dense, N, (int64_t)p + lane, r, Cs[lane], Vs[lane] * res);
+      ring.release();
     }
   }
 }
 
 template <typename T, int VPL, bool CONTIG>
 int run_sddmm(int kid, const Args& a) {
-  constexpr int words = VPL * (int)sizeof(T) / 4;
-  constexpr int U = words >= 16 ? 2 : (words >= 8 ? 4 : 8);
   const int32_t* pos = a.pos[0];
   const int32_t* crd = a.crd[0];
   const T* vals = static_cast<const T*>(a.vals[0]);
@@ -273,8 +242,10 @@ int run_sddmm(int kid, const Args& a) {
   const int64_t R = a.params[0] > 0 ? a.params[0] : 8;
   int64_t nw = a.params[1] > 0 ? a.params[1] : (R < 8 ? R : 8);
   if (nw > kMaxWarps) nw = kMaxWarps;
-  sddmm_row_kernel<T, VPL, CONTIG, U><<<(unsigned)ceil_div(M, R), (unsigned)(nw * 32), 0, a.stream>>>(
-      pos, crd, vals, Cm, Dm, out, M, N, K, R, dense);
+  constexpr int UR = VPL * (int)sizeof(T) >= 32 ? 2 : 4;  // D rows in flight per warp
+  sddmm_row_kernel<T, VPL, CONTIG, UR><<<(unsigned)ceil_div(M, R), (unsigned)(nw * 32),
+                                         (size_t)nw * LeafRing<T, 4>::kBytes, a.stream>>>(pos, crd, vals, Cm, Dm, out,
+                                                                                          M, N, K, R, dense);
   count_launch();
   return check_cuda(cudaGetLastError(), "sddmm_row_kernel");
 }
