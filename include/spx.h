@@ -199,6 +199,19 @@ int spx_selftest(uint64_t* out4, void* stream);
  * syntax); the host then runs the reference parser, which raises the exact
  * error (or accepts the literal).
  */
+/*
+ * Runtime compilation for the generic lowering fallback (generic.py): NVRTC
+ * for the current device, driver-API launch.  libnvrtc / libcuda are opened
+ * with dlopen on first use (nvrtc_path may name the library; NULL = search).
+ * spx_jit_launch takes the kernel arguments as a host array of pointers to
+ * the argument values (cuLaunchKernel's convention).
+ */
+int spx_jit_compile(const char* src, const char* kernel, const char* nvrtc_path,
+                    void** fn_out);
+int spx_jit_launch(void* fn, uint32_t grid, uint32_t block, void** args,
+                   void* stream);
+const char* spx_jit_log(void);
+
 #define SPX_PARSE_DEFER 1
 int spx_text_scan(const char* text, int64_t len, int32_t fmt, int32_t* order_out,
                   int64_t* n_out, int64_t* dims_out);

@@ -69,6 +69,9 @@ EXPORTS = (
     "spx_pack_vals",
     "spx_text_scan",
     "spx_text_parse",
+    "spx_jit_compile",
+    "spx_jit_launch",
+    "spx_jit_log",
 )
 
 
@@ -143,6 +146,12 @@ def load(path: str | os.PathLike | None = None):
     lib.spx_text_scan.restype = ctypes.c_int
     lib.spx_text_parse.argtypes = [ctypes.c_char_p, i64, ctypes.c_int32, ctypes.c_int32, i64, i64p, vp, vp]
     lib.spx_text_parse.restype = ctypes.c_int
+    lib.spx_jit_compile.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, ctypes.POINTER(vp)]
+    lib.spx_jit_compile.restype = ctypes.c_int
+    lib.spx_jit_launch.argtypes = [vp, ctypes.c_uint32, ctypes.c_uint32, ctypes.POINTER(vp), vp]
+    lib.spx_jit_launch.restype = ctypes.c_int
+    lib.spx_jit_log.argtypes = []
+    lib.spx_jit_log.restype = ctypes.c_char_p
     if path is None:
         _lib = lib
     return lib

@@ -187,6 +187,20 @@ def interpret(program: Program, inputs: dict, out_dims=None, *, dtype: str | Non
     odims = program.out_dims(dims)
     if out_dims is not None and tuple(out_dims) != tuple(odims):
         raise E.DimensionMismatchError(f"out_dims {tuple(out_dims)} but the statement produces {odims}")
+    if program.kind == "generic":
+        from . import generic
+
+        dev_out = out if (out is not None and out.device.type == "cuda") else torch.empty(
+            max(1, math.prod(odims)), dtype=torch_dtype(dtype), device=device)
+        work = generic.launch(program, ops, dev_out, dtype, _cur_stream(device))
+        stats = generic.GenericStats(program, work)
+        if out is not None:
+            if out.device.type != "cuda":
+                out.copy_(dev_out.view_as(out), non_blocking=True)
+            torch.cuda.current_stream(device).synchronize()
+            return out, stats
+        host = dev_out.cpu().numpy().astype(np.float64)[: math.prod(odims)]
+        return _spindle.tensors.DenseTensor(tuple(odims), host.reshape(odims)), stats
     sp = ops[program.ec.tensors[0]]
     if program.kind == "sddmm":
         if sparse_output is None:

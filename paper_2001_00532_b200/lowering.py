@@ -20,7 +20,8 @@ loop lowering by a table of hand-written sm_100a kernels keyed on the
 
 The result is a `Program` whose `manifest` is the reference's own
 `ir.Manifest` (ir.py:237-263) -- the parameter layout of spx_launch.  An
-unmatched shape raises the reference's `LoweringError`; there is no CPU
+unmatched shape lowers to runtime-compiled generic GPU code (generic.py), or
+raises the reference's `LoweringError` with `fallback=False`; there is no CPU
 fallback.
 """
 
@@ -521,13 +522,28 @@ def _match_mttkrp(sh: _Shape) -> Program:
     raise _NoMatch
 
 
-def lower(stmt, formats=None, dims=None) -> Program:
+def lower(stmt, formats=None, dims=None, *, fallback: bool = True):
     """Select the sm_100a kernel for a scheduled statement.
 
     Mirrors SPEC.md:370 `lower(stmt, formats, dims)`: `formats` defaults to
     the statement's own (concretize already bound them, schedule.py:340-376)
-    and `dims` (tensor name -> dims) is optional until execution.
+    and `dims` (tensor name -> dims) is optional until execution.  A shape no
+    table entry matches lowers to the generic runtime-compiled GPU code of
+    generic.py (`fallback=False` raises the LoweringError instead).
     """
+    E = _err()
+    try:
+        return _lower_table(stmt, formats, dims)
+    except E.LoweringError as err:
+        if not fallback or "disagrees with the concretized statement" in str(err):
+            raise
+        from .generic import GenericProgram, check_supported
+
+        check_supported(stmt)
+        return GenericProgram(stmt, why=str(err), dims=dict(dims) if dims is not None else None)
+
+
+def _lower_table(stmt, formats=None, dims=None) -> Program:
     E = _err()
     if formats is not None:
         fm = {}
