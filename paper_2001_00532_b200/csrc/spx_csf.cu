@@ -21,6 +21,8 @@
 //  K9 SPX_K_MTTKRP_SLICE  A.5 shape: pos(i,ipos,B)
 //     split(ipos,ipos0,ipos1,CHUNK) -> a CTA owns CHUNK slices, one warp per
 //     slice, plain stores.
+#include <type_traits>
+
 #include "spx_common.cuh"
 
 namespace spx {
@@ -141,11 +143,123 @@ struct MttkrpCtx {
   int64_t S, F, R;
 };
 
+// Paired-leaf walk for 32-wide fp32 rows (rank 32, the cfg4 shape): the two
+// half-warps take two consecutive leaves, each lane holding two columns
+// (float2), so one warp instruction reads two 128 B rows of D and one FFMA2
+// per lane covers both leaves -- half the instructions per leaf of the
+// lane-per-column walk.  The halves hold partials of the same fiber and are
+// folded with one shuffle exchange when the fiber ends.
+template <bool OWNED>
+__device__ __forceinline__ void mttkrp_walk_pair(const MttkrpCtx<float, 1, true>& c, unsigned char* ring_base,
+                                                 int lane, int q0, int q1, int f, int s) {
+  const int half = lane >> 4, hl = lane & 15;
+  const uint64_t pol_s = l2_evict_first();
+  int fb = f;
+  int fe_mine = __ldg(c.pos2 + min((int64_t)fb + 1 + lane, c.F));
+  int k_mine = __ldg(c.crd1 + min((int64_t)fb + lane, c.F - 1));
+  auto fiber_end = [&](int ff) -> int {
+    if (ff - fb >= 32) {
+      fb = ff;
+      fe_mine = __ldg(c.pos2 + min((int64_t)fb + 1 + lane, c.F));
+      k_mine = __ldg(c.crd1 + min((int64_t)fb + lane, c.F - 1));
+    }
+    return __shfl_sync(kFull, fe_mine, ff - fb);
+  };
+  auto crow_of = [&](int ff) -> float2 {
+    const int k = __shfl_sync(kFull, k_mine, ff - fb);
+    return __ldg(reinterpret_cast<const float2*>(c.Cm + (int64_t)k * 32) + hl);
+  };
+  int fend = fiber_end(f);
+  int send = __ldg(c.pos1 + s + 1);
+  float2 accf = make_float2(0.f, 0.f), accs = make_float2(0.f, 0.f);
+  float2 crow = crow_of(f);
+  auto flush_slice = [&]() {
+    if (half == 0) {
+      float* dst = c.A + (int64_t)__ldg(c.crd0 + s) * 32 + 2 * hl;
+      if constexpr (OWNED) {
+        *reinterpret_cast<float2*>(dst) = accs;
+      } else {
+        atomicAdd(dst, accs.x);
+        atomicAdd(dst + 1, accs.y);
+      }
+    }
+    accs = make_float2(0.f, 0.f);
+  };
+  auto close_fiber = [&]() {
+    float2 x = accf;
+    x.x += __shfl_xor_sync(kFull, x.x, 16);
+    x.y += __shfl_xor_sync(kFull, x.y, 16);
+    accs.x = fmaf(x.x, crow.x, accs.x);
+    accs.y = fmaf(x.y, crow.y, accs.y);
+    accf = make_float2(0.f, 0.f);
+    ++f;
+    fend = fiber_end(f);
+    while (f >= send) {
+      flush_slice();
+      ++s;
+      send = __ldg(c.pos1 + s + 1);
+    }
+    crow = crow_of(f);
+  };
+  const char* __restrict__ Dl = reinterpret_cast<const char*>(c.Dm) + hl * 8;
+  LeafRing<float, kLeafRing> ring;
+  ring.init(ring_base, c.crd2, c.vals, q0, q1);
+  ring.prologue(lane, pol_s);
+  constexpr int G = 8;  // pairs per group: 16 leaves, 8 row reads per lane in flight
+  for (int b = 0; b < ring.nb; ++b) {
+    ring.acquire(b, lane, pol_s);
+    const int p = q0 + b * 32;
+    const int n = min(32, q1 - p);
+    const int32_t* Ls = ring.crd_slot(b);
+    const float* Vs = ring.val_slot(b);
+#pragma unroll 1
+    for (int t = 0; t < n; t += 2 * G) {
+      float2 d[G];
+      float v[G];
+#pragma unroll
+      for (int u = 0; u < G; ++u) {
+        const int leaf = t + 2 * u + half;  // < 32; zero-filled past n
+        d[u] = __ldg(reinterpret_cast<const float2*>(addr_wide(Dl, (uint32_t)Ls[leaf], 128u)));
+        v[u] = Vs[leaf];
+      }
+      if (t + 2 * G <= n && p + t + 2 * G <= fend) {
+#pragma unroll
+        for (int u = 0; u < G; ++u) accf = __ffma2_rn(make_float2(v[u], v[u]), d[u], accf);
+      } else {
+#pragma unroll
+        for (int u = 0; u < G; ++u) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int leaf = t + 2 * u + h;
+            if (leaf < n) {
+              while (p + leaf >= fend) close_fiber();
+              if (half == h) accf = __ffma2_rn(make_float2(v[u], v[u]), d[u], accf);
+            }
+          }
+        }
+      }
+    }
+    ring.release();
+  }
+  float2 x = accf;
+  x.x += __shfl_xor_sync(kFull, x.x, 16);
+  x.y += __shfl_xor_sync(kFull, x.y, 16);
+  accs.x = fmaf(x.x, crow.x, accs.x);
+  accs.y = fmaf(x.y, crow.y, accs.y);
+  flush_slice();
+}
+
 // Walk leaves [q0, q1); f = fiber holding q0, s = slice holding f.
 // OWNED: the warp owns every slice it touches completely (plain stores).
 template <typename T, int VPL, bool CONTIG, bool OWNED>
 __device__ __forceinline__ void mttkrp_walk(const MttkrpCtx<T, VPL, CONTIG>& c, unsigned char* ring_base, int lane,
                                             int q0, int q1, int f, int s) {
+  if constexpr (std::is_same<T, float>::value && VPL == 1 && CONTIG) {
+    if (c.R == 32) {
+      mttkrp_walk_pair<OWNED>(c, ring_base, lane, q0, q1, f, s);
+      return;
+    }
+  }
   using Fr = Frag<T, VPL, CONTIG>;
   const int ncols = (int)c.R;
   const int Ri = (int)c.R;
