@@ -36,9 +36,10 @@ namespace {
 // lane that ends a fiber stores A[i,j] (each (i,j) is one fiber, so plain
 // stores); a fiber that continues past the batch is carried in a register.
 constexpr int kTtvRing = 8;
+constexpr int kTtvWarps = 8;
 
 template <typename T>
-__global__ void __launch_bounds__(kMaxThreads) ttv_fiber_kernel(const int32_t* __restrict__ crd0,
+__global__ void __launch_bounds__(kTtvWarps * 32) ttv_fiber_kernel(const int32_t* __restrict__ crd0,
                                                          const int32_t* __restrict__ pos1,
                                                          const int32_t* __restrict__ crd1,
                                                          const int32_t* __restrict__ pos2,
@@ -449,8 +450,11 @@ int run_ttv(const Args& a) {
   if (c.F == 0) return SPX_OK;
   const int64_t FTB = a.params[0] > 0 ? a.params[0] : 256;
   const int64_t FW = a.params[1] > 0 ? a.params[1] : 32;
-  const int64_t nw = ceil_div(FTB, FW);
-  if (nw > kMaxWarps) return fail(SPX_E_UNSUPPORTED, "TTV: FIBERS_PER_TB/FIBERS_PER_WARP must be <= 16");
+  if (ceil_div(FTB, FW) > kMaxWarps)
+    return fail(SPX_E_UNSUPPORTED, "TTV: FIBERS_PER_TB/FIBERS_PER_WARP must be <= 16");
+  // the schedule's block (FIBERS_PER_TB fibers) is a unit of work; the
+  // persistent CTAs are 8 warps that take fiber groups round-robin
+  const int64_t nw = kTtvWarps;
   const size_t cbytes = (size_t)K * sizeof(T);
   const size_t rbytes = (size_t)nw * LeafRing<T, kTtvRing>::kBytes;
   const int c_in_smem = cbytes + rbytes <= kSmemBudget ? 1 : 0;
