@@ -211,10 +211,18 @@ def main():
     from paper_2001_00532_b200.formats import DeviceTensor
     from paper_2001_00532_b200.partition import csr_shards, gather_rows
 
+    # SPX_BENCH_SHARED_GPU=1 (test only): several ranks share the visible
+    # GPUs over gloo, to exercise the N>1 path on a one-GPU machine
+    shared = os.environ.get("SPX_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     A, B = workload(args)
     N = args.ncols
@@ -267,7 +275,7 @@ def main():
     times = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     t_ms = statistics.mean(times)
     if world > 1:
-        tt = torch.tensor([t_ms], device=dev)
+        tt = torch.tensor([t_ms], device="cpu" if shared else dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_ms = float(tt.item())
 
@@ -280,7 +288,8 @@ def main():
     cb_local = compulsory_bytes(rows, A.N, N, nnz_local)
     achieved = cb_local / (statistics.mean(times) * 1e-3) / 1e9
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
-            "frac": round(achieved / hbm, 4), "traffic": load_traffic(), "peak_kind": peak_kind,
+            "frac": round(achieved / hbm, 4), "traffic": load_traffic() if world == 1 else None,
+            "peak_kind": peak_kind,
             "kernel": "spmm_nnz_kernel + carry_fixup_kernel (one spx_launch)",
             "algorithmic_bytes_per_launch": cb_local,
             # what binds this kernel: every nonzero gathers one N-wide row of B
@@ -301,22 +310,24 @@ def main():
         torch.cuda.synchronize(dev)
         dist.barrier()
         g0 = time.perf_counter()
-        full = gather_rows(out.view(rows, N), counts)
+        full = gather_rows(out.view(rows, N).cpu() if shared else out.view(rows, N), counts)
         torch.cuda.synchronize(dev)
         gather_ms = (time.perf_counter() - g0) * 1e3
         del full
 
     # e2e through the public API with pinned host inputs: every step uploads
-    # A and B, runs the launch and downloads C.  `Pipeline` overlaps step
-    # k+1's upload with step k's kernel and download (full-duplex PCIe);
-    # `interpret` (one synchronous step) is reported beside it.
+    # this rank's A (its row shard when N > 1) and B, runs the launch and
+    # downloads its C rows.  `Pipeline` overlaps step k+1's upload with step
+    # k's kernel and download (full-duplex PCIe); `interpret` (one synchronous
+    # step) is reported beside it.  N > 1: per-step time = max over ranks,
+    # bytes = sum over ranks.
     e2e = None
-    if world == 1 and args.e2e_steps > 0 and not args.profile:
+    if args.e2e_steps > 0 and not args.profile:
         from paper_2001_00532_b200.pipeline import Pipeline
 
-        hA = DeviceTensor.from_arrays((A.M, A.N), "ds", {1: A.pos}, {1: A.crd}, A.vals32, dtype="f32", pin=True)
+        hA = DeviceTensor.from_arrays((rows, A.N), "ds", {1: pos}, {1: crd}, vals, dtype="f32", pin=True)
         hB = DeviceTensor.dense(B, dtype="f32", pin=True)
-        hout = torch.empty(A.M * N, dtype=torch.float32).pin_memory()
+        hout = torch.empty(max(1, rows * N), dtype=torch.float32).pin_memory()[: rows * N]
         h2d = hA.nbytes() + hB.nbytes()
         d2h = hout.numel() * 4
         interpret(prog, {"A": hA, "B": hB}, out=hout)  # warm
@@ -337,14 +348,24 @@ def main():
         pipe.submit({"A": hA, "B": hB}, hout)  # warm
         pipe.drain()
         torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
             pipe.submit({"A": hA, "B": hB}, hout)
         pipe.drain()
         e_t = (time.perf_counter() - t0) / args.e2e_steps
+        if world > 1:
+            agg = torch.tensor([e_t, sync_t], dtype=torch.float64)
+            dist.all_reduce(agg, op=dist.ReduceOp.MAX)
+            e_t, sync_t = float(agg[0]), float(agg[1])
+            nb = torch.tensor([h2d, d2h], dtype=torch.float64)
+            dist.all_reduce(nb, op=dist.ReduceOp.SUM)
+            h2d, d2h = int(nb[0]), int(nb[1])
         e2e = {"value": round(flops / e_t / 1e9, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e_t * 1e3, 3),
-               "api": f"Pipeline(depth=2): {args.e2e_steps} steps, host wall clock / steps",
+               "api": f"Pipeline(depth=2): {args.e2e_steps} steps, host wall clock / steps"
+                      + (", max over ranks" if world > 1 else ""),
                "sync_interpret": {"value": round(flops / sync_t / 1e9, 3), "ms_per_step": round(sync_t * 1e3, 3)}}
         ref = torch.empty_like(hout)
         interpret(prog, {"A": hA, "B": hB}, out=ref)

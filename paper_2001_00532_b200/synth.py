@@ -79,10 +79,16 @@ def _load(path: Path):
 
 
 def _save(path: Path, **arrays) -> None:
-    path.parent.mkdir(parents=True, exist_ok=True)
-    tmp = path.with_suffix(".tmp.npz")
-    np.savez(tmp, **arrays)
-    os.replace(tmp, path)
+    """Atomic cache write; several processes (one per GPU rank) may build the
+    same input concurrently, so each writes its own temporary file and the
+    last rename wins (the contents are identical)."""
+    try:
+        path.parent.mkdir(parents=True, exist_ok=True)
+        tmp = path.with_name(f"{path.stem}.{os.getpid()}.tmp.npz")
+        np.savez(tmp, **arrays)
+        os.replace(tmp, path)
+    except OSError:
+        pass  # the cache is an optimisation only
 
 
 def _values(rng, n: int) -> np.ndarray:
