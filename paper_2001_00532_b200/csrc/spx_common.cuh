@@ -107,6 +107,13 @@ __device__ __forceinline__ const P* addr_wide(const P* base, uint32_t a, uint32_
   return reinterpret_cast<const P*>(r);
 }
 
+// cp.async.cg of 16 bytes, zero-filling past src_bytes (0..16)
+__device__ __forceinline__ void cp_async16_zfill(uint32_t smem_addr, const void* gptr, int src_bytes, uint64_t pol) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;" ::"r"(smem_addr), "l"(gptr),
+               "r"(src_bytes), "l"(pol)
+               : "memory");
+}
+
 // cp.async of 4 / 8 bytes (L1-allocating .ca form, the only one these sizes
 // allow) with zero-fill when src_bytes == 0 and an L2 policy.
 __device__ __forceinline__ void cp_async4(uint32_t smem_addr, const void* gptr, int src_bytes, uint64_t pol) {

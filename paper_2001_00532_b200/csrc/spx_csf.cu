@@ -7,9 +7,9 @@
 //  K7 SPX_K_TTV_FIBER   A(i,j) = B(i,j,k) * c(k):
 //     fuse(i,j,f) pos(f,fpos,B) -> fpos walks level-1 positions (fibers);
 //     split(fpos,block,..,FIBERS_PER_TB) split(..,warp,..,FIBERS_PER_WARP).
-//     A warp takes consecutive fibers; its lanes stride the fiber's leaves
-//     and fold with a shuffle tree.  Every fiber is a distinct (i,j), so the
-//     dense output (zeroed first) is written with plain stores.
+//     A warp takes FIBERS_PER_WARP consecutive fibers and reduces their
+//     leaves by key (below).  Every fiber is a distinct (i,j), so the dense
+//     output (zeroed first) is written with plain stores.
 //  K8 SPX_K_MTTKRP_NNZ  A(i,j) = B(i,k,l) * C(k,j) * D(l,j), Appendix A.6
 //     (PAPER.md:1981-2002): reorder(i,k,l,j) fuse(k,l,kl) fuse(i,kl,f)
 //     pos(f,fpos,B) split(fpos,block,..,NNZ_PER_TB) split(..,warp,nnz,
@@ -21,6 +21,7 @@
 //  K9 SPX_K_MTTKRP_SLICE  A.5 shape: pos(i,ipos,B)
 //     split(ipos,ipos0,ipos1,CHUNK) -> a CTA owns CHUNK slices, one warp per
 //     slice, plain stores.
+#include <cstdlib>
 #include <type_traits>
 
 #include "spx_common.cuh"
@@ -28,94 +29,155 @@
 namespace spx {
 namespace {
 
-// K7 TTV: persistent CTAs stage c in shared memory (when it fits) and their
-// warps take fiber groups of FIBERS_PER_WARP fibers round-robin.  A group's
-// leaves are one contiguous position range; the warp streams it 32 leaves
-// at a time (one per lane), forms v*c[k] and folds fibers with a segmented
-// shuffle scan whose head flags come from the fibers' start positions.  The
-// lane that ends a fiber stores A[i,j] (each (i,j) is one fiber, so plain
-// stores); a fiber that continues past the batch is carried in a register.
-constexpr int kTtvRing = 8;
+// K7 TTV: persistent CTAs of kTtvWarps warps stage c in shared memory (when
+// it fits); the warps take fiber groups of FIBERS_PER_WARP fibers
+// round-robin.  A group's leaves are one contiguous position range.
 constexpr int kTtvWarps = 8;
 
+// K7 TTV, reduce-by-key form: a warp takes 128 consecutive leaves per step,
+// four per lane (one 16 B vector each of coordinates and values, streamed by
+// cp.async.cg into a per-warp ring two steps ahead).  Each lane folds its
+// four products v*c[k] into the fibers they belong to; fibers that start and
+// end inside the lane are stored at once, the lane's trailing partial joins a
+// segmented warp scan (one per 128 leaves), and the lane that holds a fiber's
+// next start stores the completed sum.  Fiber starts come from the 32 fibers
+// of the group held one per lane (bit masks over the step's 128 positions).
+constexpr int kRbkSlots = 3;
+
 template <typename T>
-__global__ void __launch_bounds__(kTtvWarps * 32) ttv_fiber_kernel(const int32_t* __restrict__ crd0,
-                                                         const int32_t* __restrict__ pos1,
-                                                         const int32_t* __restrict__ crd1,
-                                                         const int32_t* __restrict__ pos2,
-                                                         const int32_t* __restrict__ crd2,
-                                                         const T* __restrict__ vals, const T* __restrict__ c,
-                                                         T* __restrict__ A, int64_t S, int64_t F, int64_t J,
-                                                         int64_t K, int64_t FW, int64_t ngroups, int c_in_smem) {
+__global__ void __launch_bounds__(kTtvWarps * 32) ttv_rbk_kernel(const int32_t* __restrict__ crd0,
+                                                      const int32_t* __restrict__ pos1,
+                                                      const int32_t* __restrict__ crd1,
+                                                      const int32_t* __restrict__ pos2,
+                                                      const int32_t* __restrict__ crd2,
+                                                      const T* __restrict__ vals, const T* __restrict__ c,
+                                                      T* __restrict__ A, int64_t S, int64_t F, int64_t J,
+                                                      int64_t K, int64_t FW, int64_t ngroups, int c_in_smem) {
+  constexpr int SLOT = 128 * (4 + (int)sizeof(T));  // coordinates then values
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  T* sc = reinterpret_cast<T*>(smem_raw + (size_t)nw * kRbkSlots * SLOT);
   if (c_in_smem) {
-    T* sc0 = reinterpret_cast<T*>(smem_raw + (size_t)(blockDim.x >> 5) * LeafRing<T, kTtvRing>::kBytes);
-    for (int64_t k = threadIdx.x; k < K; k += blockDim.x) sc0[k] = __ldg(c + k);
+    for (int64_t k = threadIdx.x; k < K; k += blockDim.x) sc[k] = __ldg(c + k);
     __syncthreads();
   }
-  const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned char* ring_base = smem_raw + (size_t)warp * LeafRing<T, kTtvRing>::kBytes;
-  T* sc = reinterpret_cast<T*>(smem_raw + (size_t)nw * LeafRing<T, kTtvRing>::kBytes);
+  unsigned char* ring = smem_raw + (size_t)warp * kRbkSlots * SLOT;
+  const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
+  __shared__ int64_t s_offs[kTtvWarps][32];
+  int64_t* offs = s_offs[warp];
   const uint64_t pol_s = l2_evict_first();
   for (int64_t g = (int64_t)blockIdx.x * nw + warp; g < ngroups; g += (int64_t)gridDim.x * nw) {
     const int gf1 = (int)min(g * FW + FW, F);
     int sl = -1;
-    // sub-groups of 32 fibers: one lane per fiber holds its start position
-    // and its output offset A[i*J + j]
     for (int f0 = (int)(g * FW); f0 < gf1; f0 += 32) {
       const int f1 = min(f0 + 32, gf1);
       const int myfib = f0 + lane;
-      const int st_mine = __ldg(pos2 + min(myfib, f1));
+      const bool is_fib = myfib < f1;
+      const int st_mine = is_fib ? __ldg(pos2 + myfib) : 0x7fffffff;
       if (sl < 0) sl = (int)warp_search_segment(pos1, 0, S, f0, lane);
       int s_mine = sl;
-      if (myfib < f1)
+      if (is_fib)
         while (__ldg(pos1 + s_mine + 1) <= myfib) ++s_mine;
-      const int64_t off_mine = myfib < f1 ? (int64_t)__ldg(crd0 + s_mine) * J + __ldg(crd1 + myfib) : 0;
+      const int64_t off_mine = is_fib ? (int64_t)__ldg(crd0 + s_mine) * J + __ldg(crd1 + myfib) : 0;
       sl = __shfl_sync(kFull, s_mine, f1 - f0 - 1);
       const int q0 = __shfl_sync(kFull, st_mine, 0), q1 = __ldg(pos2 + f1);
-      const bool is_start = myfib < f1;
-      int fcur = 0;  // fiber (relative to f0) holding position p
-      T carry = T(0);
-      LeafRing<T, kTtvRing> ring;
-      ring.init(ring_base, crd2, vals, q0, q1);
-      ring.prologue(lane, pol_s);
-      for (int b = 0; b < ring.nb; ++b) {
-        ring.acquire(b, lane, pol_s);
-        const int p = q0 + b * 32;
-        const int n = min(32, q1 - p);
-        const int kk = ring.crd_slot(b)[lane];
-        const T vv = ring.val_slot(b)[lane];
-        ring.release();
-        T x = T(0);
-        if (lane < n) x = vv * (c_in_smem ? sc[kk] : __ldg(c + kk));
-        // head flags: bit t set when position p+t starts a fiber
-        const unsigned H =
-            __reduce_or_sync(kFull, (is_start && st_mine >= p && st_mine < p + n) ? (1u << (st_mine - p)) : 0u);
-        const unsigned upto = H & (lane == 31 ? kFull : ((2u << lane) - 1u));
-        const int sstart = upto ? 31 - __clz(upto) : 0;
+      const int a0 = q0 & ~3;  // 16-byte aligned start; positions < q0 are masked
+      const int nsteps = (q1 - a0 + 127) >> 7;
+      auto issue = [&](int st) {
+        if (st < nsteps) {
+          const int p = a0 + st * 128 + 4 * lane;
+          const int k = min(max(q1 - p, 0), 4);
+          const uint32_t d = ring_s + (st % kRbkSlots) * SLOT;
+          cp_async16_zfill(d + lane * 16, k ? (const void*)(crd2 + p) : (const void*)crd2, 4 * k, pol_s);
+#pragma unroll
+          for (int h = 0; h < (int)sizeof(T) / 4; ++h) {
+            const int kk = min(max(k - h * (16 / (int)sizeof(T)), 0), 16 / (int)sizeof(T));
+            cp_async16_zfill(d + 512 + lane * 4 * (int)sizeof(T) + h * 16,
+                             kk ? (const void*)(vals + p + h * (16 / (int)sizeof(T))) : (const void*)vals,
+                             kk * (int)sizeof(T), pol_s);
+          }
+        }
+        cp_async_commit();
+      };
+      issue(0);
+      issue(1);
+      offs[lane] = off_mine;  // A offsets of this subgroup's fibers, by f - f0
+      __syncwarp();
+      int fo = f0 - 1;  // fiber open just before the current step's first position
+      T carry = T(0);   // its partial sum
+      for (int st = 0; st < nsteps; ++st) {
+        issue(st + 2);
+        cp_async_wait<2>();
+        __syncwarp();
+        const int p = a0 + st * 128;
+        const unsigned char* slot = ring + (st % kRbkSlots) * SLOT;
+        const int4 k4 = *reinterpret_cast<const int4*>(slot + lane * 16);
+        T v4[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v4[j] = reinterpret_cast<const T*>(slot + 512)[4 * lane + j];
+        __syncwarp();  // the slot is refilled two steps later
+        const int kk[4] = {k4.x, k4.y, k4.z, k4.w};
+        T x[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int pp = p + 4 * lane + j;
+          x[j] = (pp >= q0 && pp < q1) ? v4[j] * (c_in_smem ? sc[kk[j]] : __ldg(c + kk[j])) : T(0);
+        }
+        // fiber starts in [p, p+128) as a 128-bit mask, one word per 32 positions
+        const int rel = st_mine - p;
+        unsigned H[4];
+#pragma unroll
+        for (int w = 0; w < 4; ++w)
+          H[w] = __reduce_or_sync(kFull, (rel >= 32 * w && rel < 32 * w + 32) ? (1u << (rel - 32 * w)) : 0u);
+        const int wi = lane >> 3, sh = (4 * lane) & 31;
+        const unsigned hb = (H[wi] >> sh) & 0xFu;  // start flags of my four positions
+        int before = __popc(H[wi] & ((1u << sh) - 1u));
+#pragma unroll
+        for (int w = 0; w < 3; ++w) before += (w < wi) ? __popc(H[w]) : 0;
+        // lane-local fold: seg0 = products before my first start; fibers that
+        // start and end inside my four positions are stored here
+        T seg0 = T(0), run = T(0);
+        int cnt = before;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if ((hb >> j) & 1u) {
+            if (cnt > before) {
+              if (fo + cnt >= f0) A[offs[(fo + cnt - f0) & 31]] = run;
+            } else {
+              seg0 = run;
+            }
+            run = T(0);
+            ++cnt;
+          }
+          run += x[j];
+        }
+        const bool seen = hb != 0u;
+        // segmented inclusive scan of the partial leaving each lane; the
+        // step's carry enters at lane 0
+        T v = seen ? run : run + (lane == 0 ? carry : T(0));
+        bool fl = seen || lane == 0;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-          const T y = __shfl_up_sync(kFull, x, o);
-          if (lane - o >= sstart) x += y;
+          const T y = __shfl_up_sync(kFull, v, o);
+          const bool fy = __shfl_up_sync(kFull, fl, o);
+          if (lane >= o) {
+            if (!fl) v += y;
+            fl = fl || fy;
+          }
         }
-        if (!upto) x += carry;  // continues the fiber open at the previous batch
-        const int myf = fcur + __popc(upto) - (int)(H & 1u);
-        const int lastf = fcur + __popc(H) - (int)(H & 1u);
-        const int nxt = __shfl_sync(kFull, st_mine, (lastf + 1) & 31);  // start of the next fiber
-        const int lastend = lastf + 1 >= f1 - f0 ? q1 : nxt;
-        const bool ends_here = lane < n && ((lane + 1 < n && ((H >> (lane + 1)) & 1u)) ||
-                                            (lane == n - 1 && lastend == p + n));
-        const int64_t off = __shfl_sync(kFull, off_mine, myf & 31);
-        if (ends_here) A[off] = x;
-        const T tail = __shfl_sync(kFull, x, n - 1);
-        if (lastend == p + n) {
-          carry = T(0);
-          fcur = lastf + 1;
-        } else {
-          carry = tail;
-          fcur = lastf;
+        T in = __shfl_up_sync(kFull, v, 1);  // partial arriving at my first position
+        if (lane == 0) in = carry;
+        if (seen) {  // my first start completes the fiber open when my lane begins
+          const int fc = fo + before;
+          if (fc >= f0) A[offs[(fc - f0) & 31]] = in + seg0;
         }
+        carry = __shfl_sync(kFull, v, 31);
+        fo += __popc(H[0]) + __popc(H[1]) + __popc(H[2]) + __popc(H[3]);
       }
+      // the last fiber of the subgroup ends at q1
+      if (lane == 0 && fo >= f0) A[offs[(fo - f0) & 31]] = carry;
+      cp_async_wait<0>();
+      __syncwarp();
     }
   }
 }
@@ -456,10 +518,10 @@ int run_ttv(const Args& a) {
   // persistent CTAs are 8 warps that take fiber groups round-robin
   const int64_t nw = kTtvWarps;
   const size_t cbytes = (size_t)K * sizeof(T);
-  const size_t rbytes = (size_t)nw * LeafRing<T, kTtvRing>::kBytes;
+  const size_t rbytes = (size_t)nw * kRbkSlots * 128 * (4 + sizeof(T));
   const int c_in_smem = cbytes + rbytes <= kSmemBudget ? 1 : 0;
   const size_t smem = rbytes + (c_in_smem ? cbytes : 0);
-  auto kern = ttv_fiber_kernel<T>;
+  auto kern = ttv_rbk_kernel<T>;
   if (int e = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                          "cudaFuncSetAttribute"))
     return e;
@@ -473,7 +535,7 @@ int run_ttv(const Args& a) {
                                                                  static_cast<const T*>(a.vals[1]), A, c.S, c.F, J, K,
                                                                  FW, ceil_div(c.F, FW), c_in_smem);
   count_launch();
-  return check_cuda(cudaGetLastError(), "ttv_fiber_kernel");
+  return check_cuda(cudaGetLastError(), "ttv_rbk_kernel");
 }
 
 template <typename T, int VPL, bool CONTIG>
