@@ -75,25 +75,23 @@ __device__ __forceinline__ void store_zero_row(T* __restrict__ row, int lane, in
   z.store(row, lane, ncols);
 }
 
-// One batch of 32 consecutive positions held one per lane: column (with the
-// hot-row flag in bit 31, see spx_spmm_analyze) and value.
+// One batch of 32 consecutive positions held one per lane: column and value.
 template <typename T>
 struct Batch {
   int c;
   T v;
   __device__ __forceinline__ void load(const int32_t* __restrict__ crd, const T* __restrict__ vals, int idx, int end,
-                                       const uint32_t* __restrict__ hot, uint64_t pol) {
+                                       uint64_t pol) {
     c = 0;
     v = T(0);
     if (idx < end) {
       c = ld_i32_first(crd + idx, pol);
       v = ld_stream_hint(vals + idx, pol);
-      if (hot && ((__ldg(hot + (c >> 5)) >> (c & 31)) & 1u)) c |= int(0x80000000u);
     }
   }
 };
 
-// RING == 0: register double-buffered gathers (any VPL / mapping).
+// RING == 0: staged-register path (default; any VPL / mapping).
 // RING  > 0: cp.async ring of RING row slots per warp in shared memory
 //            (CONTIG rows of 16 or 32 B per lane): each lane copies and later
 //            reads back only its own 16 B pieces, so the per-lane
@@ -103,8 +101,7 @@ template <typename T, int VPL, bool CONTIG, int U, int RING>
 __global__ void __launch_bounds__(kMaxThreads, RING == 0 ? SPX_SPMM_MINB : 1) spmm_nnz_kernel(
     const int32_t* __restrict__ pos, const int32_t* __restrict__ crd, const T* __restrict__ vals,
     const T* __restrict__ B, T* __restrict__ C, int64_t M, int64_t N, int64_t nnz, int64_t TB,
-    int64_t W, int32_t* __restrict__ carry_row, T* __restrict__ carry_val, const uint32_t* __restrict__ hot,
-    const int32_t* __restrict__ first) {
+    int64_t W, int32_t* __restrict__ carry_row, T* __restrict__ carry_val, const int32_t* __restrict__ first) {
   using F = Frag<T, VPL, CONTIG>;
   constexpr int PW = 32 * VPL;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -172,9 +169,9 @@ __global__ void __launch_bounds__(kMaxThreads, RING == 0 ? SPX_SPMM_MINB : 1) sp
       const uint32_t rowstride = (uint32_t)(N * (int64_t)sizeof(T));
       const int n = qe - p;
       Batch<T> b0, b1, b2;  // batches k, k+1 (resident) and k+2 (in flight)
-      b0.load(crd, vals, p + lane, qe, nullptr, pol_s);
-      b1.load(crd, vals, p + 32 + lane, qe, nullptr, pol_s);
-      b2.load(crd, vals, p + 64 + lane, qe, nullptr, pol_s);
+      b0.load(crd, vals, p + lane, qe, pol_s);
+      b1.load(crd, vals, p + 32 + lane, qe, pol_s);
+      b2.load(crd, vals, p + 64 + lane, qe, pol_s);
       auto issue = [&](int c, int slot) {
         const char* src = Bb + (uint64_t)(uint32_t)c * rowstride;
 #pragma unroll
@@ -231,7 +228,7 @@ __global__ void __launch_bounds__(kMaxThreads, RING == 0 ? SPX_SPMM_MINB : 1) sp
         }
         b0 = b1;
         b1 = b2;
-        b2.load(crd, vals, p + base + 96 + lane, qe, nullptr, pol_s);
+        b2.load(crd, vals, p + base + 96 + lane, qe, pol_s);
       }
       cp_async_wait<0>();
     } else {
@@ -490,7 +487,6 @@ int run_spmm(int kid, const Args& a, const SpmmGeom& g) {
     const size_t head_smem = ((size_t)nw * (g.pw * sizeof(T) + sizeof(int32_t)) + 15) & ~size_t(15);
     const size_t reg_ring = (size_t)nw * LeafRing<T, 4>::kBytes;  // staged-register path
     dim3 grid((unsigned)ncta, (unsigned)g.npanels);
-    const uint32_t* hot = nullptr;
     // params[5]: B-row transport (0 = default SPX_SPMM_RING or the staged-register path, >0 = cp.async ring depth, <0 = staged-register path)
     const int ring = a.params[5] != 0 ? (a.params[5] < 0 ? 0 : a.params[5]) : ring_depth();
     if constexpr (CONTIG && (VPL * sizeof(T)) % 16 == 0) {
@@ -500,7 +496,7 @@ int run_spmm(int kid, const Args& a, const SpmmGeom& g) {
           if (int e = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                                  "cudaFuncSetAttribute"))
             return e;
-          kern<<<grid, nw * 32, smem, a.stream>>>(pos, crd, vals, B, C, M, N, nnz, TB, W, carry_row, carry_val, hot, first);
+          kern<<<grid, nw * 32, smem, a.stream>>>(pos, crd, vals, B, C, M, N, nnz, TB, W, carry_row, carry_val, first);
           return SPX_OK;
         };
         int e = ring >= 16 ? launch(spmm_nnz_kernel<T, VPL, CONTIG, U, 16>, 16)
@@ -508,11 +504,11 @@ int run_spmm(int kid, const Args& a, const SpmmGeom& g) {
         if (e) return e;
       } else {
           spmm_nnz_kernel<T, VPL, CONTIG, U, 0><<<grid, nw * 32, head_smem + reg_ring, a.stream>>>(
-            pos, crd, vals, B, C, M, N, nnz, TB, W, carry_row, carry_val, hot, first);
+            pos, crd, vals, B, C, M, N, nnz, TB, W, carry_row, carry_val, first);
       }
     } else {
       spmm_nnz_kernel<T, VPL, CONTIG, U, 0><<<grid, nw * 32, head_smem + reg_ring, a.stream>>>(
-          pos, crd, vals, B, C, M, N, nnz, TB, W, carry_row, carry_val, hot, first);
+          pos, crd, vals, B, C, M, N, nnz, TB, W, carry_row, carry_val, first);
     }
     count_launch();
     if (int e = check_cuda(cudaGetLastError(), "spmm_nnz_kernel")) return e;
