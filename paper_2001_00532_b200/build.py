@@ -2,7 +2,8 @@
 
 The shared library lands next to this file so it travels with the repo
 snapshot to the GPU box (built artefacts are git-ignored, not
-gpurun-ignored).  Objects are rebuilt only when a source or header is newer.
+gpurun-ignored).  Objects are rebuilt only when a source or header is newer, or the nvcc
+flags (SPX_NVCC_EXTRA) changed.
 """
 
 from __future__ import annotations
@@ -61,6 +62,11 @@ def _compile(src: Path, obj: Path, verbose: bool) -> None:
 
 def build(force: bool = False, verbose: bool = False) -> Path:
     OBJ.mkdir(exist_ok=True)
+    stamp = OBJ / "flags.txt"
+    flags = " ".join(ARCH + NVCC_FLAGS)
+    if not stamp.exists() or stamp.read_text() != flags:
+        force = True  # SPX_NVCC_EXTRA / SPX_PTXAS_VERBOSE changed: rebuild everything
+        stamp.write_text(flags)
     hdr_mtime = max((h.stat().st_mtime for h in _headers()), default=0.0)
     jobs = []
     objs = []

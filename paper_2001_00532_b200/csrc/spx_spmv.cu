@@ -95,38 +95,76 @@ __global__ void __launch_bounds__(kMaxThreads, 2) spmv_warp_kernel(const int32_t
   }
 }
 
-// Loads NNZ_PER_THREAD consecutive (crd, vals) with vector loads when the
-// count is a compile-time multiple of 4 and the chunk is full.
+// 256-bit streaming loads (LDG.E.256, sm_100): one lane reads one whole
+// 32 B sector per instruction.  With 16 B vectors at a 32 B (crd) or 64 B
+// (fp64 vals) lane stride every sector is requested from L2 twice -- once per
+// half -- which the cfg5 ncu capture showed as ~1.5x the compulsory L2->SM
+// sectors.  L1::no_allocate keeps the streams out of L1, which then holds
+// only x.  Same-box A/B on cfg5: 1.27 ms (16 B) -> 1.19 (256-bit, L1
+// allocating) -> 1.15 ms (256-bit, no_allocate).
+#define SPX_LD256 "ld.global.nc.L1::no_allocate"
+__device__ __forceinline__ void ld256_stream(const int32_t* p, int32_t* r) {
+  asm volatile(SPX_LD256 ".v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "l"(p));
+}
+__device__ __forceinline__ void ld256_stream(const float* p, float* r) {
+  asm volatile(SPX_LD256 ".v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]), "=f"(r[7])
+               : "l"(p));
+}
+__device__ __forceinline__ void ld256_stream(const double* p, double* r) {
+  asm volatile(SPX_LD256 ".v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3])
+               : "l"(p));
+}
+
+// One thread's NNZ_PER_THREAD consecutive (crd, vals): whole-sector 256-bit
+// loads where the per-thread bytes are a multiple of 32 (16 B vectors where
+// only of 16), when the chunk is full and the addresses are aligned (always,
+// for cudaMalloc'd arrays and NNZ_PER_WARP-aligned chunks); else scalar.
 template <typename T, int TPT>
-struct ThreadChunk {
-  int32_t c[TPT];
-  T v[TPT];
-  __device__ __forceinline__ void load(const int32_t* __restrict__ crd, const T* __restrict__ vals, int64_t a,
-                                       int n) {
-    if (TPT % 4 == 0 && n == TPT) {
+__device__ __forceinline__ void load_thread_chunk(const int32_t* __restrict__ crd, const T* __restrict__ vals,
+                                                  int a, int n, int32_t* cc, T* vv) {
+  constexpr int kC = TPT * 4, kV = TPT * (int)sizeof(T);  // bytes per thread
+  constexpr bool c256 = kC % 32 == 0, v256 = kV % 32 == 0;
+  constexpr uintptr_t kAlign = (c256 || v256) ? 31 : 15;
+  const bool vec = kC % 16 == 0 && kV % 16 == 0 && n == TPT &&
+                   (((reinterpret_cast<uintptr_t>(crd + a) | reinterpret_cast<uintptr_t>(vals + a)) & kAlign) == 0);
+  if (vec) {
+    if constexpr (c256) {
 #pragma unroll
-      for (int k = 0; k < TPT / 4; ++k) {
-        int4 q = __ldcs(reinterpret_cast<const int4*>(crd + a) + k);
-        c[4 * k] = q.x;
-        c[4 * k + 1] = q.y;
-        c[4 * k + 2] = q.z;
-        c[4 * k + 3] = q.w;
-      }
-      constexpr int per16 = 16 / (int)sizeof(T);
-#pragma unroll
-      for (int k = 0; k < TPT / per16; ++k) {
-        float4 q = __ldcs(reinterpret_cast<const float4*>(vals + a) + k);
-        *reinterpret_cast<float4*>(&v[k * per16]) = q;
-      }
+      for (int k = 0; k < TPT / 8; ++k) ld256_stream(crd + a + 8 * k, cc + 8 * k);
     } else {
 #pragma unroll
-      for (int k = 0; k < TPT; ++k) {
-        c[k] = k < n ? __ldcs(crd + a + k) : 0;
-        v[k] = k < n ? __ldcs(vals + a + k) : T(0);
+      for (int k = 0; k < TPT / 4; ++k) {
+        const int4 q = __ldcs(reinterpret_cast<const int4*>(crd + a) + k);
+        cc[4 * k] = q.x;
+        cc[4 * k + 1] = q.y;
+        cc[4 * k + 2] = q.z;
+        cc[4 * k + 3] = q.w;
       }
     }
+    if constexpr (v256) {
+      constexpr int kPer = 32 / (int)sizeof(T);
+#pragma unroll
+      for (int k = 0; k < TPT / kPer; ++k) ld256_stream(vals + a + kPer * k, vv + kPer * k);
+    } else {
+      constexpr int kPer = 16 / (int)sizeof(T);
+#pragma unroll
+      for (int k = 0; k < TPT / kPer; ++k) {
+        const float4 q = __ldcs(reinterpret_cast<const float4*>(vals + a) + k);
+        *reinterpret_cast<float4*>(&vv[kPer * k]) = q;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < TPT; ++k) {
+      cc[k] = k < n ? __ldcs(crd + a + k) : 0;
+      vv[k] = k < n ? __ldcs(vals + a + k) : T(0);
+    }
   }
-};
+}
 
 // TPT > 0: compile-time NNZ_PER_THREAD; TPT == 0: runtime `tpt`.
 template <typename T, int TPT>
@@ -164,39 +202,7 @@ __global__ void __launch_bounds__(kMaxThreads, 2) spmv_nnz_kernel(const int32_t*
   T vv[TPT > 0 ? TPT : 1];
   T xv[TPT > 0 ? TPT : 1];
   if constexpr (TPT > 0) {
-    if (TPT % 4 == 0 && n == TPT) {
-#pragma unroll
-      for (int k = 0; k < TPT / 4; ++k) {
-        const int4 q = __ldcs(reinterpret_cast<const int4*>(crd + a) + k);
-        cc[4 * k] = q.x;
-        cc[4 * k + 1] = q.y;
-        cc[4 * k + 2] = q.z;
-        cc[4 * k + 3] = q.w;
-      }
-      if constexpr (sizeof(T) == 8) {
-#pragma unroll
-        for (int k = 0; k < TPT / 2; ++k) {
-          const double2 q = __ldcs(reinterpret_cast<const double2*>(vals + a) + k);
-          vv[2 * k] = q.x;
-          vv[2 * k + 1] = q.y;
-        }
-      } else {
-#pragma unroll
-        for (int k = 0; k < TPT / 4; ++k) {
-          const float4 q = __ldcs(reinterpret_cast<const float4*>(vals + a) + k);
-          vv[4 * k] = q.x;
-          vv[4 * k + 1] = q.y;
-          vv[4 * k + 2] = q.z;
-          vv[4 * k + 3] = q.w;
-        }
-      }
-    } else {
-#pragma unroll
-      for (int k = 0; k < TPT; ++k) {
-        cc[k] = k < n ? __ldcs(crd + a + k) : 0;
-        vv[k] = k < n ? __ldcs(vals + a + k) : T(0);
-      }
-    }
+    load_thread_chunk<T, TPT>(crd, vals, a, n, cc, vv);
 #pragma unroll
     for (int k = 0; k < TPT; ++k) xv[k] = __ldg(x + cc[k]);  // cc = 0 past n: harmless
   }
@@ -342,44 +348,12 @@ __global__ void __launch_bounds__(kMaxThreads, 2) spmv_nnz_atomic_kernel(
   const int a = min(q0 + lane * tpt, q1);
   const int e = min(a + tpt, q1);
   const int n = e - a;
-  // loads first: (crd, vals) with 16 B vectors, then the x gathers
+  // loads first: (crd, vals) with 256-bit vectors, then the x gathers
   int32_t cc[TPT > 0 ? TPT : 1];
   T vv[TPT > 0 ? TPT : 1];
   T xv[TPT > 0 ? TPT : 1];
   if constexpr (TPT > 0) {
-    if (TPT % 4 == 0 && n == TPT) {
-#pragma unroll
-      for (int k = 0; k < TPT / 4; ++k) {
-        const int4 qq = __ldcs(reinterpret_cast<const int4*>(crd + a) + k);
-        cc[4 * k] = qq.x;
-        cc[4 * k + 1] = qq.y;
-        cc[4 * k + 2] = qq.z;
-        cc[4 * k + 3] = qq.w;
-      }
-      if constexpr (sizeof(T) == 8) {
-#pragma unroll
-        for (int k = 0; k < TPT / 2; ++k) {
-          const double2 qq = __ldcs(reinterpret_cast<const double2*>(vals + a) + k);
-          vv[2 * k] = qq.x;
-          vv[2 * k + 1] = qq.y;
-        }
-      } else {
-#pragma unroll
-        for (int k = 0; k < TPT / 4; ++k) {
-          const float4 qq = __ldcs(reinterpret_cast<const float4*>(vals + a) + k);
-          vv[4 * k] = qq.x;
-          vv[4 * k + 1] = qq.y;
-          vv[4 * k + 2] = qq.z;
-          vv[4 * k + 3] = qq.w;
-        }
-      }
-    } else {
-#pragma unroll
-      for (int k = 0; k < TPT; ++k) {
-        cc[k] = k < n ? __ldcs(crd + a + k) : 0;
-        vv[k] = k < n ? __ldcs(vals + a + k) : T(0);
-      }
-    }
+    load_thread_chunk<T, TPT>(crd, vals, a, n, cc, vv);
 #pragma unroll
     for (int k = 0; k < TPT; ++k) xv[k] = __ldg(x + cc[k]);  // cc = 0 past n: harmless
   }

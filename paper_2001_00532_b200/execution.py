@@ -302,6 +302,10 @@ class ExecStats:
             R = max(1, p[0])
             rows = len(pos) - 1
             blk = _segment_sums(pos, R)
+            if prog.row_divide:
+                # divide(i, ., ., n) runs exactly n outer iterations of
+                # ceil(M/n) rows (schedule.py:435-438); trailing ones may be empty
+                blk = np.concatenate([blk, np.zeros(max(0, prog.row_divide - len(blk)), np.int64)])
             name = v.get("block") or "block"
             inst[name] = blk
             loops[name] = len(blk)

@@ -117,6 +117,59 @@ def uniform_csr(M: int, N: int, nnz: int, seed: int, cache: bool = True) -> Csr:
     return _csr_from_keys(M, N, d["keys"], d["vals"])
 
 
+def geometric_row_lengths(M: int, N: int, nnz: int, base: float) -> np.ndarray:
+    """Per-row nonzero counts proportional to base**r (r = 0..M-1), summing to
+    exactly `nnz`, each capped at N columns (the excess is water-filled over
+    the uncapped rows); largest-remainder rounding, ties to the longer row."""
+    if nnz > M * N:
+        raise ValueError(f"nnz={nnz} does not fit a {M}x{N} matrix")
+    w = np.power(float(base), np.arange(M, dtype=np.float64) - (M - 1))  # max weight 1, no overflow
+    L = np.zeros(M, dtype=np.int64)
+    free = np.ones(M, dtype=bool)
+    left = nnz
+    while left > 0:
+        ideal = left * w[free] / w[free].sum()
+        if (ideal <= N - L[free]).all():
+            base_n = np.floor(ideal).astype(np.int64)
+            rem = left - int(base_n.sum())
+            if rem:
+                frac = ideal - base_n
+                order = np.lexsort((-np.nonzero(free)[0], -frac))[:rem]
+                base_n[order] += 1
+            L[free] += base_n
+            break
+        cap = free.copy()
+        cap[free] = ideal > N - L[free]
+        left -= int((N - L[cap]).sum())
+        L[cap] = N
+        free &= ~cap
+    return L
+
+
+def geometric_csr(M: int, N: int, nnz: int, base: float, seed: int) -> Csr:
+    """The §8.4 load-balance input: a fixed
+    number of nonzeros, per-row counts following a geometric law with base
+    `base` (1.0 = uniform rows), rows randomly shuffled with a seeded RNG,
+    distinct uniform columns within each row, values U[-1, 1)."""
+    rng = np.random.default_rng(seed)
+    lengths = geometric_row_lengths(M, N, nnz, base)[rng.permutation(M)]
+    dense_rows = np.nonzero(lengths * 4 > N)[0]
+    # sparse rows: draw the missing count of columns per row, drop repeats,
+    # repeat until every row is full (rejection of repeats keeps each row a
+    # uniform random subset); dense rows: a seeded permutation prefix
+    need = np.where(lengths * 4 > N, 0, lengths)
+    keys = np.zeros(0, dtype=np.int64)
+    while need.any():
+        r = np.repeat(np.arange(M, dtype=np.int64), need)
+        keys = np.sort(np.concatenate([keys, r * N + rng.integers(0, N, len(r))]))
+        keys = keys[np.concatenate([[True], keys[1:] != keys[:-1]])]
+        need = np.where(lengths * 4 > N, 0, lengths - np.bincount(keys // N, minlength=M))
+    fill = [r * N + np.sort(rng.permutation(N)[: lengths[r]]) for r in dense_rows]
+    keys = np.sort(np.concatenate([keys] + fill))
+    assert len(keys) == nnz
+    return _csr_from_keys(M, N, keys, _values(rng, nnz))
+
+
 def _rmat_level_table(a, b, c, d, levels: int):
     """Probabilities of the 4^levels quadrant paths and their (row, col) bits."""
     q = np.array([a, b, c, d], dtype=np.float64)

@@ -7,4 +7,5 @@ timeout 900 python bench.py > gpurun_out/rp_bench.json 2> gpurun_out/rp_bench.er
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/rp_launches.csv python bench.py --steps 2 --warmup 1 --profile > gpurun_out/rp_bench_under_ncu.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:spmm_nnz_kernel -s 2 -c 1 -o gpurun_out/rp_spmm -f python bench.py --profile --steps 2 --warmup 1 > gpurun_out/rp_ncu_full.log 2>&1
 timeout 1200 python tools/bench_configs.py > gpurun_out/rp_configs.jsonl 2> gpurun_out/rp_configs.err
+timeout 600 python tools/bench_loadbal.py > gpurun_out/rp_loadbal.jsonl 2> gpurun_out/rp_loadbal.err
 cat gpurun_out/rp_pytest.txt gpurun_out/rp_smoke.txt gpurun_out/rp_bench.json
