@@ -197,6 +197,7 @@ __global__ void __launch_bounds__(kTtvWarps * 32) ttv_rbk_kernel(const int32_t* 
 // strategy), a plain store for a warp that owns the whole slice.
 // ---------------------------------------------------------------------------
 constexpr int kLeafRing = 4;
+constexpr int kMttkrpThreads = 512;
 
 template <typename T, int VPL, bool CONTIG>
 struct MttkrpCtx {
@@ -289,16 +290,20 @@ __device__ __forceinline__ void mttkrp_walk_pair(const MttkrpCtx<float, 1, true>
 #pragma unroll
         for (int u = 0; u < G; ++u) accf = __ffma2_rn(make_float2(v[u], v[u]), d[u], accf);
       } else {
+        // fiber segment by fiber segment: leaves [L0, L1) of the group lie in
+        // fiber f; lane-predicated FFMA2s keep d[] in registers
+        const int cnt = min(2 * G, n - t);
+        int L0 = 0;
+        while (true) {
+          const int L1 = min(cnt, fend - (p + t));
 #pragma unroll
-        for (int u = 0; u < G; ++u) {
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int leaf = t + 2 * u + h;
-            if (leaf < n) {
-              while (p + leaf >= fend) close_fiber();
-              if (half == h) accf = __ffma2_rn(make_float2(v[u], v[u]), d[u], accf);
-            }
+          for (int u = 0; u < G; ++u) {
+            const int leaf = 2 * u + half;
+            if (leaf >= L0 && leaf < L1) accf = __ffma2_rn(make_float2(v[u], v[u]), d[u], accf);
           }
+          if (L1 >= cnt) break;
+          L0 = L1;
+          while (p + t + L0 >= fend) close_fiber();
         }
       }
     }
@@ -312,6 +317,134 @@ __device__ __forceinline__ void mttkrp_walk_pair(const MttkrpCtx<float, 1, true>
   flush_slice();
 }
 
+// Quarter-warp walk for 32-wide fp32 rows (rank 32, the cfg4 shape): the
+// four quarter-warps take four consecutive leaves, each lane holding four
+// columns (float4), so one warp instruction reads four 128 B rows of D (one
+// L1TEX wavefront each -- the floor for this op) and two FFMA2 per lane cover
+// all four leaves.  The quarters keep separate fiber and slice partials:
+// scaling by C[k,:] is linear, so sum_q(accf_q * crow) is applied per quarter
+// at each fiber end with no cross-lane traffic, and the quarters are folded
+// (two xor shuffles) only when a slice is flushed.  A group of 4*G leaves
+// inside one fiber takes 2*G FFMA2 per lane; a group that crosses fiber ends
+// runs segment by segment with the products masked (FSEL) to the segment.
+template <bool OWNED, int G>
+__device__ __forceinline__ void mttkrp_walk_quad(const MttkrpCtx<float, 1, true>& c, unsigned char* ring_base,
+                                                 int lane, int q0, int q1, int f, int s) {
+  static_assert(G == 4, "one 16 B vector of coordinates / values per quarter");
+  // fiber window: ends and k coordinates of fibers [fb, fb+32), per warp in
+  // shared memory (broadcast reads, no shuffles in the divergent close path)
+  __shared__ int s_win[kMttkrpThreads / 32][64];
+  int* win = s_win[threadIdx.x >> 5];
+  const int qw = lane >> 3, ql = lane & 7;
+  const uint64_t pol_s = l2_evict_first();
+  int fb = f;
+  auto load_win = [&]() {
+    __syncwarp();
+    win[lane] = __ldg(c.pos2 + min((int64_t)fb + 1 + lane, c.F));
+    win[32 + lane] = __ldg(c.crd1 + min((int64_t)fb + lane, c.F - 1));
+    __syncwarp();
+  };
+  load_win();
+  auto fiber_end = [&](int ff) -> int {
+    if (ff - fb >= 32) {
+      fb = ff;
+      load_win();
+    }
+    return win[ff - fb];
+  };
+  const float4* __restrict__ Cq = reinterpret_cast<const float4*>(c.Cm) + ql;
+  const float4* __restrict__ Dq = reinterpret_cast<const float4*>(c.Dm) + ql;
+  auto crow_of = [&](int ff) -> float4 { return __ldg(Cq + (uint32_t)win[32 + ff - fb] * 8u); };
+  int fend = fiber_end(f);
+  int send = __ldg(c.pos1 + s + 1);
+  float2 af0 = make_float2(0.f, 0.f), af1 = af0, as0 = af0, as1 = af0;
+  float4 crow = crow_of(f);
+  auto flush_slice = [&]() {
+    float4 x = make_float4(as0.x, as0.y, as1.x, as1.y);
+#pragma unroll
+    for (int o = 8; o < 32; o <<= 1) {
+      x.x += __shfl_xor_sync(kFull, x.x, o);
+      x.y += __shfl_xor_sync(kFull, x.y, o);
+      x.z += __shfl_xor_sync(kFull, x.z, o);
+      x.w += __shfl_xor_sync(kFull, x.w, o);
+    }
+    if (qw == 0) {
+      float4* dst = reinterpret_cast<float4*>(c.A + (int64_t)__ldg(c.crd0 + s) * 32) + ql;
+      if constexpr (OWNED) *dst = x;
+      else atomicAdd(dst, x);
+    }
+    as0 = make_float2(0.f, 0.f);
+    as1 = as0;
+  };
+  auto close_fiber = [&]() {
+    as0 = __ffma2_rn(af0, make_float2(crow.x, crow.y), as0);
+    as1 = __ffma2_rn(af1, make_float2(crow.z, crow.w), as1);
+    af0 = make_float2(0.f, 0.f);
+    af1 = af0;
+    ++f;
+    fend = fiber_end(f);
+    while (f >= send) {
+      flush_slice();
+      ++s;
+      send = __ldg(c.pos1 + s + 1);
+    }
+    crow = crow_of(f);
+  };
+  LeafRing<float, kLeafRing> ring;
+  ring.init(ring_base, c.crd2, c.vals, q0, q1);
+  ring.prologue(lane, pol_s);
+  for (int b = 0; b < ring.nb; ++b) {
+    ring.acquire(b, lane, pol_s);
+    const int p = q0 + b * 32;
+    const int n = min(32, q1 - p);
+    const int32_t* Ls = ring.crd_slot(b);
+    const float* Vs = ring.val_slot(b);
+#pragma unroll 1
+    for (int t = 0; t < n; t += 4 * G) {
+      // quarter qw takes leaves t + 4*qw .. t + 4*qw + 3 (zero-filled past n)
+      const int4 l4 = *reinterpret_cast<const int4*>(Ls + t + 4 * qw);
+      const float4 v4 = *reinterpret_cast<const float4*>(Vs + t + 4 * qw);
+      const float4 d0 = __ldg(Dq + (uint32_t)l4.x * 8u);
+      const float4 d1 = __ldg(Dq + (uint32_t)l4.y * 8u);
+      const float4 d2 = __ldg(Dq + (uint32_t)l4.z * 8u);
+      const float4 d3 = __ldg(Dq + (uint32_t)l4.w * 8u);
+#define SPX_QFMA(vv, d)                                                          \
+  do {                                                                           \
+    af0 = __ffma2_rn(make_float2((vv), (vv)), make_float2((d).x, (d).y), af0); \
+    af1 = __ffma2_rn(make_float2((vv), (vv)), make_float2((d).z, (d).w), af1); \
+  } while (0)
+      if (t + 4 * G <= n && p + t + 4 * G <= fend) {
+        SPX_QFMA(v4.x, d0);
+        SPX_QFMA(v4.y, d1);
+        SPX_QFMA(v4.z, d2);
+        SPX_QFMA(v4.w, d3);
+      } else {
+        // fiber segment by fiber segment: leaves [L0, L1) of the group lie
+        // in fiber f; products outside the segment are masked to zero
+        const int cnt = min(4 * G, n - t);
+        const int me = 4 * qw;
+        int L0 = 0;
+        while (true) {
+          const int L1 = min(cnt, fend - (p + t));
+          SPX_QFMA((me >= L0 && me < L1) ? v4.x : 0.f, d0);
+          SPX_QFMA((me + 1 >= L0 && me + 1 < L1) ? v4.y : 0.f, d1);
+          SPX_QFMA((me + 2 >= L0 && me + 2 < L1) ? v4.z : 0.f, d2);
+          SPX_QFMA((me + 3 >= L0 && me + 3 < L1) ? v4.w : 0.f, d3);
+          if (L1 >= cnt) break;
+          L0 = L1;
+          while (p + t + L0 >= fend) close_fiber();
+        }
+      }
+#undef SPX_QFMA
+    }
+    ring.release();
+  }
+  as0 = __ffma2_rn(af0, make_float2(crow.x, crow.y), as0);
+  as1 = __ffma2_rn(af1, make_float2(crow.z, crow.w), as1);
+  flush_slice();
+}
+
+
 // Walk leaves [q0, q1); f = fiber holding q0, s = slice holding f.
 // OWNED: the warp owns every slice it touches completely (plain stores).
 template <typename T, int VPL, bool CONTIG, bool OWNED>
@@ -319,7 +452,11 @@ __device__ __forceinline__ void mttkrp_walk(const MttkrpCtx<T, VPL, CONTIG>& c, 
                                             int q0, int q1, int f, int s) {
   if constexpr (std::is_same<T, float>::value && VPL == 1 && CONTIG) {
     if (c.R == 32) {
+#ifdef SPX_MTTKRP_PAIR
       mttkrp_walk_pair<OWNED>(c, ring_base, lane, q0, q1, f, s);
+#else
+      mttkrp_walk_quad<OWNED, 4>(c, ring_base, lane, q0, q1, f, s);
+#endif
       return;
     }
   }
@@ -434,7 +571,6 @@ __device__ __forceinline__ void mttkrp_walk(const MttkrpCtx<T, VPL, CONTIG>& c, 
 }
 #undef SPX_DROW
 
-constexpr int kMttkrpThreads = 512;
 constexpr size_t kSmemBudget = 200 * 1024;
 
 // K8: persistent CTAs; warp-chunk q covers leaves [q*W, (q+1)*W) (the
