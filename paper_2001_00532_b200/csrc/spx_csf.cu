@@ -34,17 +34,25 @@ namespace {
 // round-robin.  A group's leaves are one contiguous position range.
 constexpr int kTtvWarps = 8;
 
-// K7 TTV, reduce-by-key form: a warp takes 128 consecutive leaves per step,
-// four per lane (one 16 B vector each of coordinates and values, streamed by
-// cp.async.cg into a per-warp ring two steps ahead).  Each lane folds its
-// four products v*c[k] into the fibers they belong to; fibers that start and
+// K7 TTV, reduce-by-key form: a warp takes 32*LPL consecutive leaves per
+// step, LPL per lane (whole 16 B vectors of coordinates and values, streamed
+// by cp.async.cg into a per-warp ring two steps ahead).  Each lane folds its
+// LPL products v*c[k] into the fibers they belong to; fibers that start and
 // end inside the lane are stored at once, the lane's trailing partial joins a
-// segmented warp scan (one per 128 leaves), and the lane that holds a fiber's
-// next start stores the completed sum.  Fiber starts come from the 32 fibers
-// of the group held one per lane (bit masks over the step's 128 positions).
+// segmented warp scan (one per step), and the lane that holds a fiber's next
+// start stores the completed sum.  Fiber starts come from the 32 fibers of
+// the group held one per lane (bit masks over the step's positions, one
+// 32-bit word per 32 positions); every per-lane array is indexed at compile
+// time.  LPL is a tuning knob: same-box A/B on cfg4 gave 0.45 / 0.51 / 0.72 ms
+// for LPL = 4 / 8 / 16 -- larger steps amortise the scan but the bigger ring
+// slots cost occupancy, which this latency-bound loop needs more.
 constexpr int kRbkSlots = 3;
+#ifndef SPX_TTV_LPL
+#define SPX_TTV_LPL 4
+#endif
+constexpr int kTtvLpl = SPX_TTV_LPL;
 
-template <typename T>
+template <typename T, int LPL>
 __global__ void __launch_bounds__(kTtvWarps * 32) ttv_rbk_kernel(const int32_t* __restrict__ crd0,
                                                       const int32_t* __restrict__ pos1,
                                                       const int32_t* __restrict__ crd1,
@@ -53,7 +61,11 @@ __global__ void __launch_bounds__(kTtvWarps * 32) ttv_rbk_kernel(const int32_t* 
                                                       const T* __restrict__ vals, const T* __restrict__ c,
                                                       T* __restrict__ A, int64_t S, int64_t F, int64_t J,
                                                       int64_t K, int64_t FW, int64_t ngroups, int c_in_smem) {
-  constexpr int SLOT = 128 * (4 + (int)sizeof(T));  // coordinates then values
+  static_assert(LPL % 4 == 0 && LPL <= 32, "whole int4 coordinate vectors per lane");
+  constexpr int STEP = 32 * LPL;                       // leaves per warp step
+  constexpr int SLOT = STEP * (4 + (int)sizeof(T));    // coordinates then values
+  constexpr int VCH = LPL * (int)sizeof(T) / 16;       // 16 B value chunks per lane
+  constexpr int VPC = 16 / (int)sizeof(T);             // values per chunk
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   T* sc = reinterpret_cast<T*>(smem_raw + (size_t)nw * kRbkSlots * SLOT);
@@ -82,64 +94,84 @@ __global__ void __launch_bounds__(kTtvWarps * 32) ttv_rbk_kernel(const int32_t* 
       sl = __shfl_sync(kFull, s_mine, f1 - f0 - 1);
       const int q0 = __shfl_sync(kFull, st_mine, 0), q1 = __ldg(pos2 + f1);
       const int a0 = q0 & ~3;  // 16-byte aligned start; positions < q0 are masked
-      const int nsteps = (q1 - a0 + 127) >> 7;
-      auto issue = [&](int st) {
+      const int nsteps = (q1 - a0 + STEP - 1) / STEP;
+      auto issue = [&](int st, int slot_i) {
         if (st < nsteps) {
-          const int p = a0 + st * 128 + 4 * lane;
-          const int k = min(max(q1 - p, 0), 4);
-          const uint32_t d = ring_s + (st % kRbkSlots) * SLOT;
-          cp_async16_zfill(d + lane * 16, k ? (const void*)(crd2 + p) : (const void*)crd2, 4 * k, pol_s);
+          const int p = a0 + st * STEP + LPL * lane;
+          const uint32_t d = ring_s + slot_i * SLOT;
 #pragma unroll
-          for (int h = 0; h < (int)sizeof(T) / 4; ++h) {
-            const int kk = min(max(k - h * (16 / (int)sizeof(T)), 0), 16 / (int)sizeof(T));
-            cp_async16_zfill(d + 512 + lane * 4 * (int)sizeof(T) + h * 16,
-                             kk ? (const void*)(vals + p + h * (16 / (int)sizeof(T))) : (const void*)vals,
-                             kk * (int)sizeof(T), pol_s);
+          for (int h = 0; h < LPL / 4; ++h) {
+            const int k = min(max(q1 - (p + 4 * h), 0), 4);
+            cp_async16_zfill(d + (lane * LPL + 4 * h) * 4, k ? (const void*)(crd2 + p + 4 * h) : (const void*)crd2,
+                             4 * k, pol_s);
+          }
+#pragma unroll
+          for (int h = 0; h < VCH; ++h) {
+            const int kk = min(max(q1 - (p + h * VPC), 0), VPC);
+            cp_async16_zfill(d + STEP * 4 + (lane * LPL + h * VPC) * (int)sizeof(T),
+                             kk ? (const void*)(vals + p + h * VPC) : (const void*)vals, kk * (int)sizeof(T), pol_s);
           }
         }
         cp_async_commit();
       };
-      issue(0);
-      issue(1);
+      issue(0, 0);
+      issue(1, 1);
       offs[lane] = off_mine;  // A offsets of this subgroup's fibers, by f - f0
       __syncwarp();
       int fo = f0 - 1;  // fiber open just before the current step's first position
       T carry = T(0);   // its partial sum
+      int slot_i = 0;   // st % kRbkSlots
       for (int st = 0; st < nsteps; ++st) {
-        issue(st + 2);
+        issue(st + 2, slot_i == 0 ? 2 : slot_i - 1);
         cp_async_wait<2>();
         __syncwarp();
-        const int p = a0 + st * 128;
-        const unsigned char* slot = ring + (st % kRbkSlots) * SLOT;
-        const int4 k4 = *reinterpret_cast<const int4*>(slot + lane * 16);
-        T v4[4];
+        const int p = a0 + st * STEP;
+        const unsigned char* slot = ring + slot_i * SLOT;
+        slot_i = slot_i == kRbkSlots - 1 ? 0 : slot_i + 1;
+        int kk[LPL];
+        T v[LPL];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) v4[j] = reinterpret_cast<const T*>(slot + 512)[4 * lane + j];
-        __syncwarp();  // the slot is refilled two steps later
-        const int kk[4] = {k4.x, k4.y, k4.z, k4.w};
-        T x[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int pp = p + 4 * lane + j;
-          x[j] = (pp >= q0 && pp < q1) ? v4[j] * (c_in_smem ? sc[kk[j]] : __ldg(c + kk[j])) : T(0);
+        for (int h = 0; h < LPL / 4; ++h) {
+          const int4 k4 = *reinterpret_cast<const int4*>(slot + (lane * LPL + 4 * h) * 4);
+          kk[4 * h] = k4.x;
+          kk[4 * h + 1] = k4.y;
+          kk[4 * h + 2] = k4.z;
+          kk[4 * h + 3] = k4.w;
         }
-        // fiber starts in [p, p+128) as a 128-bit mask, one word per 32 positions
+#pragma unroll
+        for (int j = 0; j < LPL; ++j) v[j] = reinterpret_cast<const T*>(slot + STEP * 4)[LPL * lane + j];
+        __syncwarp();  // the slot is refilled two steps later
+        T x[LPL];
+#pragma unroll
+        for (int j = 0; j < LPL; ++j) {
+          const int pp = p + LPL * lane + j;
+          x[j] = (pp >= q0 && pp < q1) ? v[j] * (c_in_smem ? sc[kk[j]] : __ldg(c + kk[j])) : T(0);
+        }
+        // fiber starts in [p, p+STEP) as a bit mask, one word per 32 positions
         const int rel = st_mine - p;
-        unsigned H[4];
+        const int rw = (rel >= 0 && rel < STEP) ? (rel >> 5) : -1;
+        const unsigned rbit = 1u << (rel & 31);
+        constexpr int kLanesPerWord = 32 / LPL;
+        const int wi = lane / kLanesPerWord, sh = (LPL * lane) & 31;
+        unsigned myw = 0u;
+        int before = 0, total = 0;
 #pragma unroll
-        for (int w = 0; w < 4; ++w)
-          H[w] = __reduce_or_sync(kFull, (rel >= 32 * w && rel < 32 * w + 32) ? (1u << (rel - 32 * w)) : 0u);
-        const int wi = lane >> 3, sh = (4 * lane) & 31;
-        const unsigned hb = (H[wi] >> sh) & 0xFu;  // start flags of my four positions
-        int before = __popc(H[wi] & ((1u << sh) - 1u));
-#pragma unroll
-        for (int w = 0; w < 3; ++w) before += (w < wi) ? __popc(H[w]) : 0;
+        for (int w = 0; w < LPL; ++w) {
+          const unsigned Hw = __reduce_or_sync(kFull, rw == w ? rbit : 0u);
+          const int pc = __popc(Hw);
+          before += (w < wi) ? pc : 0;
+          total += pc;
+          myw = (w == wi) ? Hw : myw;
+        }
+        constexpr unsigned kLaneMask = LPL == 32 ? 0xffffffffu : ((1u << LPL) - 1u);
+        const unsigned hb = (myw >> sh) & kLaneMask;  // start flags of my LPL positions
+        before += __popc(myw & ((1u << sh) - 1u));
         // lane-local fold: seg0 = products before my first start; fibers that
-        // start and end inside my four positions are stored here
+        // start and end inside my positions are stored here
         T seg0 = T(0), run = T(0);
         int cnt = before;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < LPL; ++j) {
           if ((hb >> j) & 1u) {
             if (cnt > before) {
               if (fo + cnt >= f0) A[offs[(fo + cnt - f0) & 31]] = run;
@@ -154,25 +186,25 @@ __global__ void __launch_bounds__(kTtvWarps * 32) ttv_rbk_kernel(const int32_t* 
         const bool seen = hb != 0u;
         // segmented inclusive scan of the partial leaving each lane; the
         // step's carry enters at lane 0
-        T v = seen ? run : run + (lane == 0 ? carry : T(0));
+        T vs = seen ? run : run + (lane == 0 ? carry : T(0));
         bool fl = seen || lane == 0;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-          const T y = __shfl_up_sync(kFull, v, o);
+          const T y = __shfl_up_sync(kFull, vs, o);
           const bool fy = __shfl_up_sync(kFull, fl, o);
           if (lane >= o) {
-            if (!fl) v += y;
+            if (!fl) vs += y;
             fl = fl || fy;
           }
         }
-        T in = __shfl_up_sync(kFull, v, 1);  // partial arriving at my first position
+        T in = __shfl_up_sync(kFull, vs, 1);  // partial arriving at my first position
         if (lane == 0) in = carry;
         if (seen) {  // my first start completes the fiber open when my lane begins
           const int fc = fo + before;
           if (fc >= f0) A[offs[(fc - f0) & 31]] = in + seg0;
         }
-        carry = __shfl_sync(kFull, v, 31);
-        fo += __popc(H[0]) + __popc(H[1]) + __popc(H[2]) + __popc(H[3]);
+        carry = __shfl_sync(kFull, vs, 31);
+        fo += total;
       }
       // the last fiber of the subgroup ends at q1
       if (lane == 0 && fo >= f0) A[offs[(fo - f0) & 31]] = carry;
@@ -198,6 +230,14 @@ __global__ void __launch_bounds__(kTtvWarps * 32) ttv_rbk_kernel(const int32_t* 
 // ---------------------------------------------------------------------------
 constexpr int kLeafRing = 4;
 constexpr int kMttkrpThreads = 512;
+// tuning knobs (same-box A/B on cfg4: G=4 with 2 CTAs/SM 1.24-1.26 ms; G=8 or
+// 1 CTA/SM 1.63-1.65 ms -- occupancy wins over per-warp ILP here)
+#ifndef SPX_MTTKRP_G
+#define SPX_MTTKRP_G 4
+#endif
+#ifndef SPX_MTTKRP_MINB
+#define SPX_MTTKRP_MINB 2
+#endif
 
 template <typename T, int VPL, bool CONTIG>
 struct MttkrpCtx {
@@ -206,116 +246,6 @@ struct MttkrpCtx {
   T* A;
   int64_t S, F, R;
 };
-
-// Paired-leaf walk for 32-wide fp32 rows (rank 32, the cfg4 shape): the two
-// half-warps take two consecutive leaves, each lane holding two columns
-// (float2), so one warp instruction reads two 128 B rows of D and one FFMA2
-// per lane covers both leaves -- half the instructions per leaf of the
-// lane-per-column walk.  The halves hold partials of the same fiber and are
-// folded with one shuffle exchange when the fiber ends.
-template <bool OWNED>
-__device__ __forceinline__ void mttkrp_walk_pair(const MttkrpCtx<float, 1, true>& c, unsigned char* ring_base,
-                                                 int lane, int q0, int q1, int f, int s) {
-  const int half = lane >> 4, hl = lane & 15;
-  const uint64_t pol_s = l2_evict_first();
-  int fb = f;
-  int fe_mine = __ldg(c.pos2 + min((int64_t)fb + 1 + lane, c.F));
-  int k_mine = __ldg(c.crd1 + min((int64_t)fb + lane, c.F - 1));
-  auto fiber_end = [&](int ff) -> int {
-    if (ff - fb >= 32) {
-      fb = ff;
-      fe_mine = __ldg(c.pos2 + min((int64_t)fb + 1 + lane, c.F));
-      k_mine = __ldg(c.crd1 + min((int64_t)fb + lane, c.F - 1));
-    }
-    return __shfl_sync(kFull, fe_mine, ff - fb);
-  };
-  auto crow_of = [&](int ff) -> float2 {
-    const int k = __shfl_sync(kFull, k_mine, ff - fb);
-    return __ldg(reinterpret_cast<const float2*>(c.Cm + (int64_t)k * 32) + hl);
-  };
-  int fend = fiber_end(f);
-  int send = __ldg(c.pos1 + s + 1);
-  float2 accf = make_float2(0.f, 0.f), accs = make_float2(0.f, 0.f);
-  float2 crow = crow_of(f);
-  auto flush_slice = [&]() {
-    if (half == 0) {
-      float* dst = c.A + (int64_t)__ldg(c.crd0 + s) * 32 + 2 * hl;
-      if constexpr (OWNED) {
-        *reinterpret_cast<float2*>(dst) = accs;
-      } else {
-        atomicAdd(dst, accs.x);
-        atomicAdd(dst + 1, accs.y);
-      }
-    }
-    accs = make_float2(0.f, 0.f);
-  };
-  auto close_fiber = [&]() {
-    float2 x = accf;
-    x.x += __shfl_xor_sync(kFull, x.x, 16);
-    x.y += __shfl_xor_sync(kFull, x.y, 16);
-    accs.x = fmaf(x.x, crow.x, accs.x);
-    accs.y = fmaf(x.y, crow.y, accs.y);
-    accf = make_float2(0.f, 0.f);
-    ++f;
-    fend = fiber_end(f);
-    while (f >= send) {
-      flush_slice();
-      ++s;
-      send = __ldg(c.pos1 + s + 1);
-    }
-    crow = crow_of(f);
-  };
-  const char* __restrict__ Dl = reinterpret_cast<const char*>(c.Dm) + hl * 8;
-  LeafRing<float, kLeafRing> ring;
-  ring.init(ring_base, c.crd2, c.vals, q0, q1);
-  ring.prologue(lane, pol_s);
-  constexpr int G = 8;  // pairs per group: 16 leaves, 8 row reads per lane in flight
-  for (int b = 0; b < ring.nb; ++b) {
-    ring.acquire(b, lane, pol_s);
-    const int p = q0 + b * 32;
-    const int n = min(32, q1 - p);
-    const int32_t* Ls = ring.crd_slot(b);
-    const float* Vs = ring.val_slot(b);
-#pragma unroll 1
-    for (int t = 0; t < n; t += 2 * G) {
-      float2 d[G];
-      float v[G];
-#pragma unroll
-      for (int u = 0; u < G; ++u) {
-        const int leaf = t + 2 * u + half;  // < 32; zero-filled past n
-        d[u] = __ldg(reinterpret_cast<const float2*>(addr_wide(Dl, (uint32_t)Ls[leaf], 128u)));
-        v[u] = Vs[leaf];
-      }
-      if (t + 2 * G <= n && p + t + 2 * G <= fend) {
-#pragma unroll
-        for (int u = 0; u < G; ++u) accf = __ffma2_rn(make_float2(v[u], v[u]), d[u], accf);
-      } else {
-        // fiber segment by fiber segment: leaves [L0, L1) of the group lie in
-        // fiber f; lane-predicated FFMA2s keep d[] in registers
-        const int cnt = min(2 * G, n - t);
-        int L0 = 0;
-        while (true) {
-          const int L1 = min(cnt, fend - (p + t));
-#pragma unroll
-          for (int u = 0; u < G; ++u) {
-            const int leaf = 2 * u + half;
-            if (leaf >= L0 && leaf < L1) accf = __ffma2_rn(make_float2(v[u], v[u]), d[u], accf);
-          }
-          if (L1 >= cnt) break;
-          L0 = L1;
-          while (p + t + L0 >= fend) close_fiber();
-        }
-      }
-    }
-    ring.release();
-  }
-  float2 x = accf;
-  x.x += __shfl_xor_sync(kFull, x.x, 16);
-  x.y += __shfl_xor_sync(kFull, x.y, 16);
-  accs.x = fmaf(x.x, crow.x, accs.x);
-  accs.y = fmaf(x.y, crow.y, accs.y);
-  flush_slice();
-}
 
 // Quarter-warp walk for 32-wide fp32 rows (rank 32, the cfg4 shape): the
 // four quarter-warps take four consecutive leaves, each lane holding four
@@ -330,7 +260,7 @@ __device__ __forceinline__ void mttkrp_walk_pair(const MttkrpCtx<float, 1, true>
 template <bool OWNED, int G>
 __device__ __forceinline__ void mttkrp_walk_quad(const MttkrpCtx<float, 1, true>& c, unsigned char* ring_base,
                                                  int lane, int q0, int q1, int f, int s) {
-  static_assert(G == 4, "one 16 B vector of coordinates / values per quarter");
+  static_assert(G == 4 || G == 8, "whole 16 B vectors of coordinates / values per quarter");
   // fiber window: ends and k coordinates of fibers [fb, fb+32), per warp in
   // shared memory (broadcast reads, no shuffles in the divergent close path)
   __shared__ int s_win[kMttkrpThreads / 32][64];
@@ -401,35 +331,40 @@ __device__ __forceinline__ void mttkrp_walk_quad(const MttkrpCtx<float, 1, true>
     const float* Vs = ring.val_slot(b);
 #pragma unroll 1
     for (int t = 0; t < n; t += 4 * G) {
-      // quarter qw takes leaves t + 4*qw .. t + 4*qw + 3 (zero-filled past n)
-      const int4 l4 = *reinterpret_cast<const int4*>(Ls + t + 4 * qw);
-      const float4 v4 = *reinterpret_cast<const float4*>(Vs + t + 4 * qw);
-      const float4 d0 = __ldg(Dq + (uint32_t)l4.x * 8u);
-      const float4 d1 = __ldg(Dq + (uint32_t)l4.y * 8u);
-      const float4 d2 = __ldg(Dq + (uint32_t)l4.z * 8u);
-      const float4 d3 = __ldg(Dq + (uint32_t)l4.w * 8u);
+      // quarter qw takes leaves t + G*qw .. t + G*qw + G-1 (zero-filled past n)
+      float4 d[G];
+      float v[G];
+#pragma unroll
+      for (int h = 0; h < G / 4; ++h) {
+        const int4 l4 = *reinterpret_cast<const int4*>(Ls + t + G * qw + 4 * h);
+        const float4 v4 = *reinterpret_cast<const float4*>(Vs + t + G * qw + 4 * h);
+        d[4 * h] = __ldg(Dq + (uint32_t)l4.x * 8u);
+        d[4 * h + 1] = __ldg(Dq + (uint32_t)l4.y * 8u);
+        d[4 * h + 2] = __ldg(Dq + (uint32_t)l4.z * 8u);
+        d[4 * h + 3] = __ldg(Dq + (uint32_t)l4.w * 8u);
+        v[4 * h] = v4.x;
+        v[4 * h + 1] = v4.y;
+        v[4 * h + 2] = v4.z;
+        v[4 * h + 3] = v4.w;
+      }
 #define SPX_QFMA(vv, d)                                                          \
   do {                                                                           \
     af0 = __ffma2_rn(make_float2((vv), (vv)), make_float2((d).x, (d).y), af0); \
     af1 = __ffma2_rn(make_float2((vv), (vv)), make_float2((d).z, (d).w), af1); \
   } while (0)
       if (t + 4 * G <= n && p + t + 4 * G <= fend) {
-        SPX_QFMA(v4.x, d0);
-        SPX_QFMA(v4.y, d1);
-        SPX_QFMA(v4.z, d2);
-        SPX_QFMA(v4.w, d3);
+#pragma unroll
+        for (int u = 0; u < G; ++u) SPX_QFMA(v[u], d[u]);
       } else {
         // fiber segment by fiber segment: leaves [L0, L1) of the group lie
         // in fiber f; products outside the segment are masked to zero
         const int cnt = min(4 * G, n - t);
-        const int me = 4 * qw;
+        const int me = G * qw;
         int L0 = 0;
         while (true) {
           const int L1 = min(cnt, fend - (p + t));
-          SPX_QFMA((me >= L0 && me < L1) ? v4.x : 0.f, d0);
-          SPX_QFMA((me + 1 >= L0 && me + 1 < L1) ? v4.y : 0.f, d1);
-          SPX_QFMA((me + 2 >= L0 && me + 2 < L1) ? v4.z : 0.f, d2);
-          SPX_QFMA((me + 3 >= L0 && me + 3 < L1) ? v4.w : 0.f, d3);
+#pragma unroll
+          for (int u = 0; u < G; ++u) SPX_QFMA((me + u >= L0 && me + u < L1) ? v[u] : 0.f, d[u]);
           if (L1 >= cnt) break;
           L0 = L1;
           while (p + t + L0 >= fend) close_fiber();
@@ -452,11 +387,7 @@ __device__ __forceinline__ void mttkrp_walk(const MttkrpCtx<T, VPL, CONTIG>& c, 
                                             int q0, int q1, int f, int s) {
   if constexpr (std::is_same<T, float>::value && VPL == 1 && CONTIG) {
     if (c.R == 32) {
-#ifdef SPX_MTTKRP_PAIR
-      mttkrp_walk_pair<OWNED>(c, ring_base, lane, q0, q1, f, s);
-#else
-      mttkrp_walk_quad<OWNED, 4>(c, ring_base, lane, q0, q1, f, s);
-#endif
+      mttkrp_walk_quad<OWNED, SPX_MTTKRP_G>(c, ring_base, lane, q0, q1, f, s);
       return;
     }
   }
@@ -576,7 +507,7 @@ constexpr size_t kSmemBudget = 200 * 1024;
 // K8: persistent CTAs; warp-chunk q covers leaves [q*W, (q+1)*W) (the
 // schedule's `warp` variable; NNZ_PER_TB/NNZ_PER_WARP chunks make a `block`).
 template <typename T, int VPL, bool CONTIG>
-__global__ void __launch_bounds__(kMttkrpThreads, 2) mttkrp_nnz_kernel(
+__global__ void __launch_bounds__(kMttkrpThreads, SPX_MTTKRP_MINB) mttkrp_nnz_kernel(
     const int32_t* __restrict__ crd0, const int32_t* __restrict__ pos1, const int32_t* __restrict__ crd1,
     const int32_t* __restrict__ pos2, const int32_t* __restrict__ crd2, const T* __restrict__ vals,
     const T* __restrict__ Cm, const T* __restrict__ Dm, T* __restrict__ A, int64_t S, int64_t F, int64_t nnz,
@@ -654,10 +585,10 @@ int run_ttv(const Args& a) {
   // persistent CTAs are 8 warps that take fiber groups round-robin
   const int64_t nw = kTtvWarps;
   const size_t cbytes = (size_t)K * sizeof(T);
-  const size_t rbytes = (size_t)nw * kRbkSlots * 128 * (4 + sizeof(T));
+  const size_t rbytes = (size_t)nw * kRbkSlots * 32 * kTtvLpl * (4 + sizeof(T));
   const int c_in_smem = cbytes + rbytes <= kSmemBudget ? 1 : 0;
   const size_t smem = rbytes + (c_in_smem ? cbytes : 0);
-  auto kern = ttv_rbk_kernel<T>;
+  auto kern = ttv_rbk_kernel<T, kTtvLpl>;
   if (int e = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                          "cudaFuncSetAttribute"))
     return e;
