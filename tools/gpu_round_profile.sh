@@ -8,4 +8,5 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:spmm_nnz_kernel -s 2 -c 1 -o gpurun_out/rp_spmm -f python bench.py --profile --steps 2 --warmup 1 > gpurun_out/rp_ncu_full.log 2>&1
 timeout 1200 python tools/bench_configs.py > gpurun_out/rp_configs.jsonl 2> gpurun_out/rp_configs.err
 timeout 600 python tools/bench_loadbal.py > gpurun_out/rp_loadbal.jsonl 2> gpurun_out/rp_loadbal.err
+timeout 900 python tools/bench_shards.py > gpurun_out/rp_shards.jsonl 2> gpurun_out/rp_shards.err
 cat gpurun_out/rp_pytest.txt gpurun_out/rp_smoke.txt gpurun_out/rp_bench.json
