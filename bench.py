@@ -307,13 +307,20 @@ def main():
         counts = [0] * world
         shards = csr_shards(A.pos, A.crd, A.vals32, world)
         counts = [s.row1 - s.row0 for s in shards]
+        comm = None
+        if not shared:
+            from paper_2001_00532_b200.comm import Comm
+
+            comm = Comm.from_process_group()  # libspx NCCL communicator (spx_comm_init)
         torch.cuda.synchronize(dev)
         dist.barrier()
         g0 = time.perf_counter()
-        full = gather_rows(out.view(rows, N).cpu() if shared else out.view(rows, N), counts)
+        full = gather_rows(out.view(rows, N).cpu() if shared else out.view(rows, N), counts, comm=comm)
         torch.cuda.synchronize(dev)
         gather_ms = (time.perf_counter() - g0) * 1e3
         del full
+        if comm is not None:
+            comm.close()
 
     # e2e through the public API with pinned host inputs: every step uploads
     # this rank's A (its row shard when N > 1) and B, runs the launch and

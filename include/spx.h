@@ -62,6 +62,7 @@ extern "C" {
  * BASELINE configs 2-4 are fp32) */
 #define SPX_F64 0
 #define SPX_F32 1
+#define SPX_I32 2 /* collectives only */
 
 /*
  * Kernel ids -- one per row of the schedule-shape selection table
@@ -155,6 +156,36 @@ int spx_partition(const int32_t* seg_start, int64_t nseg, int64_t nnz,
  * int64 array of ndev+1 entries. */
 int spx_partition_device(const int32_t* seg_start, int64_t nseg, int64_t nnz,
                          int32_t ndev, int64_t* bounds_out, void* stream);
+
+/*
+ * Multi-GPU collectives (SURVEY.md §8(b) "spx_comm_init / spx_gather /
+ * spx_reduce_rows"; §8(e)): NCCL over NVLink on caller streams, opened with
+ * dlopen (libnccl.so.2) so the library has no link-time NCCL dependency and
+ * shares the process's NCCL when the host runtime has already loaded it.  The
+ * reference has no multi-GPU path; these carry the data-path gathers.
+ *
+ * spx_comm_available: 1 when libnccl could be opened.
+ * spx_comm_unique_id: 128-byte ncclUniqueId into id_out (rank 0; the host
+ *   broadcasts it over its own process-group store).
+ * spx_comm_init: one communicator per process (rank = global rank; the
+ *   current CUDA device is the rank's GPU).
+ * spx_comm_init_all: ndev communicators in one process (comms_out[ndev]);
+ *   issue their collectives between spx_comm_group(1) and spx_comm_group(0).
+ * spx_gather: all-gather of `count` elements per rank (each rank's row shard
+ *   padded to the largest), rank-major into recv[nranks*count].
+ * spx_reduce_rows: element-wise sum over ranks (in place when send == recv),
+ *   for the partial outputs of leaf-exact CSF shards (MTTKRP/TTV).
+ * dtype: SPX_F64, SPX_F32 or SPX_I32.
+ */
+int spx_comm_available(void);
+int spx_comm_unique_id(void* id_out);
+int spx_comm_init(int nranks, int rank, const void* id, void** comm_out);
+int spx_comm_init_all(int ndev, const int* devs, void** comms_out);
+int spx_comm_destroy(void* comm);
+int spx_comm_info(void* comm, int* nranks, int* rank);
+int spx_comm_group(int begin);
+int spx_gather(void* comm, const void* send, void* recv, size_t count, int dtype, void* stream);
+int spx_reduce_rows(void* comm, const void* send, void* recv, size_t count, int dtype, void* stream);
 
 /* Device self-test: writes the createpolicy.fractional L2::evict_last /
  * evict_first descriptors of this GPU and the constants the kernels use in

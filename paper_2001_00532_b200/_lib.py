@@ -26,6 +26,7 @@ SPX_E_WORKSPACE = 6
 
 SPX_F64 = 0
 SPX_F32 = 1
+SPX_I32 = 2
 
 K_SPMV_ROW = 1
 K_SPMV_WARP = 2
@@ -72,6 +73,15 @@ EXPORTS = (
     "spx_jit_compile",
     "spx_jit_launch",
     "spx_jit_log",
+    "spx_comm_available",
+    "spx_comm_unique_id",
+    "spx_comm_init",
+    "spx_comm_init_all",
+    "spx_comm_destroy",
+    "spx_comm_info",
+    "spx_comm_group",
+    "spx_gather",
+    "spx_reduce_rows",
 )
 
 
@@ -152,6 +162,25 @@ def load(path: str | os.PathLike | None = None):
     lib.spx_jit_launch.restype = ctypes.c_int
     lib.spx_jit_log.argtypes = []
     lib.spx_jit_log.restype = ctypes.c_char_p
+    ip = ctypes.POINTER(ctypes.c_int)
+    lib.spx_comm_available.argtypes = []
+    lib.spx_comm_available.restype = ctypes.c_int
+    lib.spx_comm_unique_id.argtypes = [vp]
+    lib.spx_comm_unique_id.restype = ctypes.c_int
+    lib.spx_comm_init.argtypes = [ctypes.c_int, ctypes.c_int, vp, ctypes.POINTER(vp)]
+    lib.spx_comm_init.restype = ctypes.c_int
+    lib.spx_comm_init_all.argtypes = [ctypes.c_int, ip, ctypes.POINTER(vp)]
+    lib.spx_comm_init_all.restype = ctypes.c_int
+    lib.spx_comm_destroy.argtypes = [vp]
+    lib.spx_comm_destroy.restype = ctypes.c_int
+    lib.spx_comm_info.argtypes = [vp, ip, ip]
+    lib.spx_comm_info.restype = ctypes.c_int
+    lib.spx_comm_group.argtypes = [ctypes.c_int]
+    lib.spx_comm_group.restype = ctypes.c_int
+    lib.spx_gather.argtypes = [vp, vp, vp, sz, ctypes.c_int, vp]
+    lib.spx_gather.restype = ctypes.c_int
+    lib.spx_reduce_rows.argtypes = [vp, vp, vp, sz, ctypes.c_int, vp]
+    lib.spx_reduce_rows.restype = ctypes.c_int
     if path is None:
         _lib = lib
     return lib

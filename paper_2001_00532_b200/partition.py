@@ -18,8 +18,10 @@ other rank's, so SpMV/SpMM/SDDMM need only a final gather.
 straddle ranks); MTTKRP/TTV then finish with the partial-result reduction
 (`reduce_partials`, an all-reduce of the small dense output).
 
-Collectives go through torch.distributed (NCCL over NVLink on the GPU box,
-gloo in the CPU tests); the data path of a shard never communicates.
+Collectives: on the GPU the gather / reduction is one libspx NCCL call
+(`comm.Comm`, spx_gather / spx_reduce_rows); without a Comm (the CPU tests)
+they go through torch.distributed over gloo.  The data path of a shard never
+communicates.
 """
 
 from __future__ import annotations
@@ -133,24 +135,35 @@ def csf_shards(pos: dict, crd: dict, vals: np.ndarray, ndev: int, exact: bool = 
 # -- collectives ---------------------------------------------------------------
 
 
-def gather_rows(local: torch.Tensor, row_counts: list[int], group=None) -> torch.Tensor:
+def gather_rows(local: torch.Tensor, row_counts: list[int], group=None, comm=None) -> torch.Tensor:
     """All-gather variable-size row shards (dim 0) into the full output on
-    every rank (torch.distributed; NCCL on GPUs, gloo on CPU)."""
-    import torch.distributed as dist
-
-    world = dist.get_world_size(group)
+    every rank.  With a libspx `comm.Comm` and CUDA tensors this is one
+    spx_gather (NCCL all-gather on the current stream); otherwise
+    torch.distributed (gloo in the CPU tests)."""
     mx = max(row_counts) if row_counts else 0
     tail = tuple(local.shape[1:])
     pad = torch.zeros((mx,) + tail, dtype=local.dtype, device=local.device)
     if local.shape[0]:
         pad[: local.shape[0]] = local
-    bufs = [torch.empty_like(pad) for _ in range(world)]
-    dist.all_gather(bufs, pad, group=group)
+    if comm is not None and local.is_cuda:
+        world = comm.nranks
+        flat = torch.empty((world * mx,) + tail, dtype=local.dtype, device=local.device)
+        comm.all_gather(pad, flat)
+        bufs = list(flat.split(mx)) if mx else [flat[:0]] * world
+    else:
+        import torch.distributed as dist
+
+        world = dist.get_world_size(group)
+        bufs = [torch.empty_like(pad) for _ in range(world)]
+        dist.all_gather(bufs, pad, group=group)
     return torch.cat([b[:n] for b, n in zip(bufs, row_counts)], dim=0)
 
 
-def reduce_partials(partial: torch.Tensor, group=None) -> torch.Tensor:
-    """Partial-result reduction for slices split across ranks (MTTKRP/TTV)."""
+def reduce_partials(partial: torch.Tensor, group=None, comm=None) -> torch.Tensor:
+    """Partial-result reduction for slices split across ranks (MTTKRP/TTV):
+    spx_reduce_rows with a `comm.Comm` on the GPU, else torch.distributed."""
+    if comm is not None and partial.is_cuda:
+        return comm.all_reduce(partial)
     import torch.distributed as dist
 
     dist.all_reduce(partial, op=dist.ReduceOp.SUM, group=group)

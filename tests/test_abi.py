@@ -131,3 +131,9 @@ def test_csf_shards_preserve_mttkrp(exact):
     for p in parts:
         acc += O.mttkrp(T.dims, p.pos, p.crd, p.vals, C, D)
     assert np.allclose(acc, full, rtol=1e-12, atol=1e-12)
+
+
+def test_comm_available_is_safe_without_a_gpu():
+    from paper_2001_00532_b200 import _lib
+
+    assert _lib.load().spx_comm_available() in (0, 1)
