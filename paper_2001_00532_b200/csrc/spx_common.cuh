@@ -127,6 +127,26 @@ __device__ __forceinline__ void cp_async8(uint32_t smem_addr, const void* gptr, 
                : "memory");
 }
 
+// 16 bytes of ELEM-byte elements of which the first `nvalid` exist: one
+// 16 B cp.async when the chunk is whole, else one cp.async per element with
+// zero-fill, so no byte past the last element is read (compute-sanitizer
+// initcheck counts a partial 16 B copy as a 16 B read of the tail).
+template <int ELEM>
+__device__ __forceinline__ void cp_async16_elems(uint32_t smem_addr, const void* gptr, int nvalid, uint64_t pol) {
+  static_assert(ELEM == 4 || ELEM == 8, "4 or 8 byte elements");
+  if (nvalid * ELEM >= 16) {
+    cp_async16_zfill(smem_addr, gptr, 16, pol);
+  } else {
+    const char* g = static_cast<const char*>(gptr);
+#pragma unroll
+    for (int e = 0; e < 16 / ELEM; ++e) {
+      const bool ok = e < nvalid;
+      if constexpr (ELEM == 4) cp_async4(smem_addr + 4 * e, ok ? g + 4 * e : g, ok ? 4 : 0, pol);
+      else cp_async8(smem_addr + 8 * e, ok ? g + 8 * e : g, ok ? 8 : 0, pol);
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Per-warp ring of leaf batches: (crd, val) of 32 consecutive positions per
 // slot, streamed from HBM into shared memory by cp.async RING-1 batches

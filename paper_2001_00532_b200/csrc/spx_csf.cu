@@ -47,20 +47,24 @@ constexpr int kTtvWarps = 8;
 // for LPL = 4 / 8 / 16 -- larger steps amortise the scan but the bigger ring
 // slots cost occupancy, which this latency-bound loop needs more.
 constexpr int kRbkSlots = 3;
+#ifndef SPX_TTV_MINB
+#define SPX_TTV_MINB 6  // 40 registers: 6 CTAs (48 warps) per SM; occupancy-bound
+#endif
 #ifndef SPX_TTV_LPL
 #define SPX_TTV_LPL 4
 #endif
 constexpr int kTtvLpl = SPX_TTV_LPL;
 
 template <typename T, int LPL>
-__global__ void __launch_bounds__(kTtvWarps * 32) ttv_rbk_kernel(const int32_t* __restrict__ crd0,
+__global__ void __launch_bounds__(kTtvWarps * 32, SPX_TTV_MINB) ttv_rbk_kernel(const int32_t* __restrict__ crd0,
                                                       const int32_t* __restrict__ pos1,
                                                       const int32_t* __restrict__ crd1,
                                                       const int32_t* __restrict__ pos2,
                                                       const int32_t* __restrict__ crd2,
                                                       const T* __restrict__ vals, const T* __restrict__ c,
                                                       T* __restrict__ A, int64_t S, int64_t F, int64_t J,
-                                                      int64_t K, int64_t FW, int64_t ngroups, int c_in_smem) {
+                                                      int64_t K, int64_t FW, int64_t ngroups, int c_in_smem,
+                                                      int nnz) {
   static_assert(LPL % 4 == 0 && LPL <= 32, "whole int4 coordinate vectors per lane");
   constexpr int STEP = 32 * LPL;                       // leaves per warp step
   constexpr int SLOT = STEP * (4 + (int)sizeof(T));    // coordinates then values
@@ -99,17 +103,28 @@ __global__ void __launch_bounds__(kTtvWarps * 32) ttv_rbk_kernel(const int32_t* 
         if (st < nsteps) {
           const int p = a0 + st * STEP + LPL * lane;
           const uint32_t d = ring_s + slot_i * SLOT;
+          // whole 16 B copies wherever the step lies inside the arrays: positions
+          // past q1 are masked in the fold, so only the arrays' end needs care
+          if (a0 + (st + 1) * STEP <= nnz) {  // warp-uniform
 #pragma unroll
-          for (int h = 0; h < LPL / 4; ++h) {
-            const int k = min(max(q1 - (p + 4 * h), 0), 4);
-            cp_async16_zfill(d + (lane * LPL + 4 * h) * 4, k ? (const void*)(crd2 + p + 4 * h) : (const void*)crd2,
-                             4 * k, pol_s);
-          }
+            for (int h = 0; h < LPL / 4; ++h)
+              cp_async16_zfill(d + (lane * LPL + 4 * h) * 4, crd2 + p + 4 * h, 16, pol_s);
 #pragma unroll
-          for (int h = 0; h < VCH; ++h) {
-            const int kk = min(max(q1 - (p + h * VPC), 0), VPC);
-            cp_async16_zfill(d + STEP * 4 + (lane * LPL + h * VPC) * (int)sizeof(T),
-                             kk ? (const void*)(vals + p + h * VPC) : (const void*)vals, kk * (int)sizeof(T), pol_s);
+            for (int h = 0; h < VCH; ++h)
+              cp_async16_zfill(d + STEP * 4 + (lane * LPL + h * VPC) * (int)sizeof(T), vals + p + h * VPC, 16, pol_s);
+          } else {  // the arrays' last step: nothing past q1 is read
+#pragma unroll
+            for (int h = 0; h < LPL / 4; ++h) {
+              const int k = min(max(q1 - (p + 4 * h), 0), 4);
+              cp_async16_elems<4>(d + (lane * LPL + 4 * h) * 4,
+                                  k ? (const void*)(crd2 + p + 4 * h) : (const void*)crd2, k, pol_s);
+            }
+#pragma unroll
+            for (int h = 0; h < VCH; ++h) {
+              const int kk = min(max(q1 - (p + h * VPC), 0), VPC);
+              cp_async16_elems<(int)sizeof(T)>(d + STEP * 4 + (lane * LPL + h * VPC) * (int)sizeof(T),
+                                               kk ? (const void*)(vals + p + h * VPC) : (const void*)vals, kk, pol_s);
+            }
           }
         }
         cp_async_commit();
@@ -600,7 +615,7 @@ int run_ttv(const Args& a) {
   kern<<<(unsigned)grid, (unsigned)(nw * 32), smem, a.stream>>>(c.crd0, c.pos1, c.crd1, c.pos2, c.crd2,
                                                                  static_cast<const T*>(a.vals[0]),
                                                                  static_cast<const T*>(a.vals[1]), A, c.S, c.F, J, K,
-                                                                 FW, ceil_div(c.F, FW), c_in_smem);
+                                                                 FW, ceil_div(c.F, FW), c_in_smem, (int)c.nnz);
   count_launch();
   return check_cuda(cudaGetLastError(), "ttv_rbk_kernel");
 }
