@@ -16,6 +16,11 @@
 //     same batch pipeline one row at a time.
 #include "spx_common.cuh"
 
+// tuning knob: 3 CTAs/SM forces 40 registers and spills 48-280 B per thread
+#ifndef SPX_SDDMM_MINB
+#define SPX_SDDMM_MINB 2
+#endif
+
 namespace spx {
 namespace {
 
@@ -61,7 +66,7 @@ __device__ __forceinline__ T transpose_reduce8(T (&part)[8], int lane) {
 // products folded by transpose_reduce8, and the 32 results of a batch
 // stored coalesced by the lanes that own them.
 template <typename T, int VPL, bool CONTIG, int U>
-__global__ void __launch_bounds__(kMaxThreads, 2) sddmm_nnz_kernel(const int32_t* __restrict__ pos,
+__global__ void __launch_bounds__(kMaxThreads, SPX_SDDMM_MINB) sddmm_nnz_kernel(const int32_t* __restrict__ pos,
                                                             const int32_t* __restrict__ crd,
                                                             const T* __restrict__ vals, const T* __restrict__ Cm,
                                                             const T* __restrict__ Dm, T* __restrict__ out, int64_t M,

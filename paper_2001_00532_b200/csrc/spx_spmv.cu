@@ -332,8 +332,12 @@ __global__ void __launch_bounds__(kMaxThreads, 2) spmv_nnz_kernel(const int32_t*
 // may differ in the last bits from run to run (atomic order).
 constexpr int kWarpPos = 320;  // pos entries staged per warp
 
+// tuning knob: 3 CTAs/SM forces 40 registers and spills (cfg5 1.32 vs 1.15 ms)
+#ifndef SPX_SPMV_MINB
+#define SPX_SPMV_MINB 2
+#endif
 template <typename T, int TPT>
-__global__ void __launch_bounds__(kMaxThreads, 2) spmv_nnz_atomic_kernel(
+__global__ void __launch_bounds__(kMaxThreads, SPX_SPMV_MINB) spmv_nnz_atomic_kernel(
     const int32_t* __restrict__ pos, const int32_t* __restrict__ crd, const T* __restrict__ vals,
     const T* __restrict__ x, T* __restrict__ y, int64_t M, int64_t nnz, int64_t W, int tpt_rt,
     const int32_t* __restrict__ first) {
