@@ -244,7 +244,10 @@ __global__ void __launch_bounds__(kTtvWarps * 32, SPX_TTV_MINB) ttv_rbk_kernel(c
 // strategy), a plain store for a warp that owns the whole slice.
 // ---------------------------------------------------------------------------
 constexpr int kLeafRing = 4;
-constexpr int kMttkrpThreads = 512;
+#ifndef SPX_MTTKRP_THREADS
+#define SPX_MTTKRP_THREADS 512
+#endif
+constexpr int kMttkrpThreads = SPX_MTTKRP_THREADS;
 // tuning knobs (same-box A/B on cfg4: G=4 with 2 CTAs/SM 1.24-1.26 ms; G=8 or
 // 1 CTA/SM 1.63-1.65 ms -- occupancy wins over per-warp ILP here)
 #ifndef SPX_MTTKRP_G
