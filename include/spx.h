@@ -254,6 +254,13 @@ int spx_pack_sort(const int32_t* const* coords_host, int32_t order,
                   const int64_t* dims, int64_t n, const double* vals,
                   void* ws, size_t ws_bytes, int32_t* ucoords, double* uvals,
                   int64_t* info, void* stream);
+/* Same, with level l's i-th coordinate at coords_host[l][i * coord_stride]
+ * (coord_stride = order for one row-major (n, order) array, no copies). */
+int spx_pack_sort_strided(const int32_t* const* coords_host, int64_t coord_stride,
+                          int32_t order, const int64_t* dims, int64_t n,
+                          const double* vals, void* ws, size_t ws_bytes,
+                          int32_t* ucoords, double* uvals, int64_t* info,
+                          void* stream);
 size_t spx_pack_level_workspace_size(int64_t nu);
 int spx_pack_level(const int32_t* ucoord, int64_t nu, int32_t compressed,
                    int64_t dim, int64_t parent_count, int64_t* diff,

@@ -64,6 +64,7 @@ EXPORTS = (
     "spx_selftest",
     "spx_pack_workspace_size",
     "spx_pack_sort",
+    "spx_pack_sort_strided",
     "spx_pack_level_workspace_size",
     "spx_pack_level",
     "spx_pack_level_fill",
@@ -144,6 +145,8 @@ def load(path: str | os.PathLike | None = None):
     lib.spx_pack_workspace_size.restype = sz
     lib.spx_pack_sort.argtypes = [ctypes.POINTER(vp), ctypes.c_int32, i64p, i64, vp, vp, sz, vp, vp, vp, vp]
     lib.spx_pack_sort.restype = ctypes.c_int
+    lib.spx_pack_sort_strided.argtypes = [ctypes.POINTER(vp), i64, ctypes.c_int32, i64p, i64, vp, vp, sz, vp, vp, vp, vp]
+    lib.spx_pack_sort_strided.restype = ctypes.c_int
     lib.spx_pack_level_workspace_size.argtypes = [i64]
     lib.spx_pack_level_workspace_size.restype = sz
     lib.spx_pack_level.argtypes = [vp, i64, ctypes.c_int32, i64, i64, vp, vp, vp, vp, sz, vp, vp]

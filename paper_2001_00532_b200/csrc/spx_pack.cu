@@ -279,8 +279,8 @@ struct DimsArg {
   int order;
 };
 
-__global__ void pack_keys_kernel(DimsArg dims, const int32_t* const* __restrict__ coords, int64_t n,
-                                 uint64_t* __restrict__ keys, uint32_t* __restrict__ idx,
+__global__ void pack_keys_kernel(DimsArg dims, const int32_t* const* __restrict__ coords, int64_t stride,
+                                 int64_t n, uint64_t* __restrict__ keys, uint32_t* __restrict__ idx,
                                  unsigned long long* __restrict__ first_bad) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -289,7 +289,7 @@ __global__ void pack_keys_kernel(DimsArg dims, const int32_t* const* __restrict_
 #pragma unroll
   for (int l = 0; l < 8; ++l) {  // static indices: DimsArg stays in the parameter bank
     if (l < dims.order) {
-      const int64_t c = coords[l][i];
+      const int64_t c = coords[l][i * stride];
       bad |= c < 0 || c >= dims.d[l];
       k = k * (uint64_t)dims.d[l] + (uint64_t)c;
     }
@@ -408,9 +408,10 @@ size_t spx_pack_workspace_size(int64_t n, int32_t order) {
   return pack_layout(n).total;
 }
 
-int spx_pack_sort(const int32_t* const* coords_host, int32_t order, const int64_t* dims, int64_t n,
-                  const double* vals, void* ws, size_t ws_bytes, int32_t* ucoords, double* uvals, int64_t* info,
-                  void* stream) {
+int spx_pack_sort_strided(const int32_t* const* coords_host, int64_t coord_stride, int32_t order,
+                          const int64_t* dims, int64_t n, const double* vals, void* ws, size_t ws_bytes,
+                          int32_t* ucoords, double* uvals, int64_t* info, void* stream) {
+  if (coord_stride < 1) return fail(SPX_E_ARG, "spx_pack_sort: coordinate stride %lld", (long long)coord_stride);
   if (order < 1 || order > 8 || n < 0 || !dims || !info) return fail(SPX_E_ARG, "spx_pack_sort: bad arguments");
   if (n > 0 && (!coords_host || !vals || !ucoords || !uvals)) return fail(SPX_E_ARG, "spx_pack_sort: null buffer");
   if (n > (int64_t)UINT32_MAX) return fail(SPX_E_UNSUPPORTED, "spx_pack_sort: more than 2^32 entries");
@@ -451,7 +452,7 @@ int spx_pack_sort(const int32_t* const* coords_host, int32_t order, const int64_
   if (int e = check_cuda(cudaMemcpyAsync(dcoords, coords_host, order * sizeof(void*), cudaMemcpyHostToDevice, s),
                          "cudaMemcpyAsync"))
     return e;
-  pack_keys_kernel<<<blocks_for(n), 256, 0, s>>>(da, dcoords, n, keys, idx,
+  pack_keys_kernel<<<blocks_for(n), 256, 0, s>>>(da, dcoords, coord_stride, n, keys, idx,
                                                  reinterpret_cast<unsigned long long*>(info + 1));
   count_launch();
   if (int e = check_cuda(cudaGetLastError(), "pack_keys_kernel")) return e;
@@ -477,6 +478,12 @@ int spx_pack_sort(const int32_t* const* coords_host, int32_t order, const int64_
   unique_fold_kernel<<<blocks_for(n), 256, 0, s>>>(keys, idx, flags, ex, n, vals, da, ucoords, uvals, info);
   count_launch();
   return check_cuda(cudaGetLastError(), "unique_fold_kernel");
+}
+
+int spx_pack_sort(const int32_t* const* coords_host, int32_t order, const int64_t* dims, int64_t n,
+                  const double* vals, void* ws, size_t ws_bytes, int32_t* ucoords, double* uvals, int64_t* info,
+                  void* stream) {
+  return spx_pack_sort_strided(coords_host, 1, order, dims, n, vals, ws, ws_bytes, ucoords, uvals, info, stream);
 }
 
 int spx_pack_level(const int32_t* ucoord, int64_t nu, int32_t compressed, int64_t dim, int64_t parent_count,

@@ -58,7 +58,7 @@ def pack_device(dims, levels, coords, values, *, device=None, dtype: str = "f64"
         # values outside int32 are out of bounds for any int32-indexed level
         big = (c < -(2**31)) | (c >= 2**31)
         c = torch.where(big, torch.full_like(c, -1), c).to(torch.int32)
-    cols = [c[:, lvl].contiguous() for lvl in range(order)]
+    c = c.contiguous()  # row-major (n, order): level l is c[:, l] at stride `order`, read in place
     v = v.to(device=device, dtype=torch.float64).contiguous()
     stream = torch.cuda.current_stream(device).cuda_stream
 
@@ -66,10 +66,11 @@ def pack_device(dims, levels, coords, values, *, device=None, dtype: str = "f64"
     ucoords = torch.empty((order, max(1, n)), dtype=torch.int32, device=device)
     uvals = torch.empty(max(1, n), dtype=torch.float64, device=device)
     info = torch.empty(2, dtype=torch.int64, device=device)
-    ctab = _lib.ptr_array([t.data_ptr() for t in cols])
+    ctab = _lib.ptr_array([c.data_ptr() + 4 * lvl for lvl in range(order)])
     dims_arr = (ctypes.c_int64 * order)(*dims)
-    _lib.check(lib.spx_pack_sort(ctab, order, dims_arr, n, _ptr(v) if n else None, ws.data_ptr(), ws.numel(),
-                                 ucoords.data_ptr(), uvals.data_ptr(), info.data_ptr(), stream), "spx_pack_sort")
+    _lib.check(lib.spx_pack_sort_strided(ctab, order, order, dims_arr, n, _ptr(v) if n else None, ws.data_ptr(),
+                                         ws.numel(), ucoords.data_ptr(), uvals.data_ptr(), info.data_ptr(), stream),
+               "spx_pack_sort")
     nu, first_bad = (int(x) for x in info.cpu().tolist())
     if first_bad >= 0:
         coord = tuple(int(x) for x in c[first_bad].tolist())
