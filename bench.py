@@ -224,6 +224,15 @@ def main():
         else:
             dist.init_process_group("nccl", device_id=dev)
 
+    # libspx NCCL communicator (spx_comm_init) for the output gather and the
+    # replicated-B upload of the e2e pipeline; torch.distributed carries only
+    # its unique id and the barriers
+    comm = None
+    if world > 1 and not shared:
+        from paper_2001_00532_b200.comm import Comm
+
+        comm = Comm.from_process_group()
+
     A, B = workload(args)
     N = args.ncols
     bound = math.ceil(N / 32)
@@ -307,11 +316,6 @@ def main():
         counts = [0] * world
         shards = csr_shards(A.pos, A.crd, A.vals32, world)
         counts = [s.row1 - s.row0 for s in shards]
-        comm = None
-        if not shared:
-            from paper_2001_00532_b200.comm import Comm
-
-            comm = Comm.from_process_group()  # libspx NCCL communicator (spx_comm_init)
         torch.cuda.synchronize(dev)
         dist.barrier()
         g0 = time.perf_counter()
@@ -319,8 +323,6 @@ def main():
         torch.cuda.synchronize(dev)
         gather_ms = (time.perf_counter() - g0) * 1e3
         del full
-        if comm is not None:
-            comm.close()
 
     # e2e through the public API with pinned host inputs: every step uploads
     # this rank's A (its row shard when N > 1) and B, runs the launch and
@@ -351,7 +353,10 @@ def main():
         assert torch.equal(hout.view(-1), out.cpu().view(-1)), "e2e result differs from the device path"
         del ex, out  # free HBM for the pipeline's two slots
         torch.cuda.empty_cache()
-        pipe = Pipeline(prog, {"A": hA, "B": hB}, hout, dtype="f32", depth=2, device=dev)
+        # N > 1: each rank uploads 1/N of B's rows and an NVLink all-gather
+        # assembles the rest (every rank's A shard needs all of B)
+        pipe = Pipeline(prog, {"A": hA, "B": hB}, hout, dtype="f32", depth=2, device=dev,
+                        replicated={"B": comm} if comm is not None else None)
         pipe.submit({"A": hA, "B": hB}, hout)  # warm
         pipe.drain()
         torch.cuda.synchronize(dev)
@@ -362,17 +367,20 @@ def main():
             pipe.submit({"A": hA, "B": hB}, hout)
         pipe.drain()
         e_t = (time.perf_counter() - t0) / args.e2e_steps
+        h2d = pipe.h2d_bytes  # this rank's A shard + (N > 1) its share of B
         if world > 1:
-            agg = torch.tensor([e_t, sync_t], dtype=torch.float64)
+            red_dev = "cpu" if shared else dev  # NCCL reduces device tensors only
+            agg = torch.tensor([e_t, sync_t], dtype=torch.float64, device=red_dev)
             dist.all_reduce(agg, op=dist.ReduceOp.MAX)
             e_t, sync_t = float(agg[0]), float(agg[1])
-            nb = torch.tensor([h2d, d2h], dtype=torch.float64)
+            nb = torch.tensor([h2d, d2h], dtype=torch.float64, device=red_dev)
             dist.all_reduce(nb, op=dist.ReduceOp.SUM)
             h2d, d2h = int(nb[0]), int(nb[1])
         e2e = {"value": round(flops / e_t / 1e9, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e_t * 1e3, 3),
                "api": f"Pipeline(depth=2): {args.e2e_steps} steps, host wall clock / steps"
-                      + (", max over ranks" if world > 1 else ""),
+                      + (", max over ranks" if world > 1 else "")
+                      + (", B uploaded as 1/N row shares + NCCL all-gather (spx_gather)" if comm is not None else ""),
                "sync_interpret": {"value": round(flops / sync_t / 1e9, 3), "ms_per_step": round(sync_t * 1e3, 3)}}
         ref = torch.empty_like(hout)
         interpret(prog, {"A": hA, "B": hB}, out=ref)
@@ -402,6 +410,8 @@ def main():
         if gather_ms is not None:
             line["gather_ms"] = round(gather_ms, 3)
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
     if world > 1:
         dist.destroy_process_group()
 

@@ -51,18 +51,33 @@ class Pipeline:
     download stream."""
 
     def __init__(self, program: Program, like: dict, out_like: torch.Tensor, *, dtype: str, depth: int = 2,
-                 device=None):
+                 device=None, replicated: dict | None = None):
+        """`replicated` maps a dense operand name to a `comm.Comm`: every rank
+        needs that operand whole (SpMM's B under a row partition of A), so
+        each step uploads only this rank's 1/nranks of its rows over PCIe and
+        an NCCL all-gather over NVLink assembles the rest (spx_gather)."""
         E = _spindle.errors
         if not torch.cuda.is_available():
             raise E.ExecutionError("Pipeline needs a CUDA device (there is no CPU fallback)")
         self.device = torch.device(device or "cuda")
         self.depth = max(1, int(depth))
         self.program = program
+        self.replicated = dict(replicated or {})
         self.slots = []
         for _ in range(self.depth):
             ops = {name: _empty_like_on(t, self.device) for name, t in like.items()}
+            full = {}
+            for name, comm in self.replicated.items():
+                t = ops[name]
+                if t.pos or t.crd:
+                    raise E.ExecutionError(f"replicated operand {name!r} must be dense")
+                n = t.vals.numel()
+                chunk = -(-n // comm.nranks)
+                buf = torch.empty(chunk * comm.nranks, dtype=t.vals.dtype, device=self.device)
+                t.vals = buf[:n]  # the Executor binds the first n elements
+                full[name] = (buf, chunk)
             out = torch.empty(out_like.numel(), dtype=torch_dtype(dtype), device=self.device)
-            self.slots.append((ops, out, Executor(program, ops, out, dtype=dtype)))
+            self.slots.append((ops, out, Executor(program, ops, out, dtype=dtype), full))
         self.up = torch.cuda.Stream(self.device)
         self.compute = torch.cuda.Stream(self.device)
         self.down = torch.cuda.Stream(self.device)
@@ -76,13 +91,23 @@ class Pipeline:
         download into `out` (pinned host tensor).  Returns the event that
         marks the step's download complete."""
         s = self.k % self.depth
-        ops, dev_out, ex = self.slots[s]
+        ops, dev_out, ex, full = self.slots[s]
         with torch.cuda.stream(self.up):
             if self.free[s] is not None:
                 self.up.wait_event(self.free[s])
             nb = 0
             for name, t in inputs.items():
-                nb += _copy_into(ops[name], t)
+                if name in full:
+                    comm = self.replicated[name]
+                    buf, chunk = full[name]
+                    src = t.vals.reshape(-1)
+                    lo = min(comm.rank * chunk, src.numel())
+                    hi = min(lo + chunk, src.numel())
+                    buf[lo:hi].copy_(src[lo:hi], non_blocking=True)
+                    nb += (hi - lo) * src.element_size()
+                    comm.all_gather(buf[comm.rank * chunk:(comm.rank + 1) * chunk], buf, stream=self.up)
+                else:
+                    nb += _copy_into(ops[name], t)
             uploaded = torch.cuda.Event()
             uploaded.record(self.up)
         self.compute.wait_event(uploaded)

@@ -56,3 +56,30 @@ def test_pipeline_spmv_f64(cuda):
         pipe.submit({"A": hA, "x": hx}, out)
     pipe.drain()
     assert rel_err(out.numpy(), O.spmv(A.pos, A.crd, A.vals, x)) <= 1e-12
+
+
+def test_pipeline_replicated_operand_over_comm(cuda):
+    """B uploaded as this rank's row share and all-gathered (spx_gather): on a
+    one-rank communicator the share is all of B, and the results are the
+    plain pipeline's."""
+    from paper_2001_00532_b200.comm import Comm
+
+    A = synth.rmat_csr(10, 8_000, seed=6, cache=False)
+    prog = lower(corpus.build("A4", NNZ_PER_TB=512, NNZ_PER_WARP=64, BOUND=1))
+    rng = np.random.default_rng(9)
+    vals = rng.uniform(-1, 1, A.nnz).astype(np.float32)
+    hA = DeviceTensor.from_arrays((A.M, A.N), "ds", {1: A.pos}, {1: A.crd}, vals, dtype="f32", pin=True)
+    Bs = [rng.uniform(-1, 1, (A.N, 24)).astype(np.float32) for _ in range(3)]
+    hBs = [DeviceTensor.dense(B, dtype="f32", pin=True) for B in Bs]
+    outs = [torch.empty(A.M * 24, dtype=torch.float32).pin_memory() for _ in Bs]
+    with Comm.single() as comm:
+        pipe = Pipeline(prog, {"A": hA, "B": hBs[0]}, outs[0], dtype="f32", depth=2, device=cuda,
+                        replicated={"B": comm})
+        for hB, out in zip(hBs, outs):
+            pipe.submit({"A": hA, "B": hB}, out)
+        pipe.drain()
+    for hB, out in zip(hBs, outs):
+        ref = torch.empty_like(out)
+        interpret(prog, {"A": hA, "B": hB}, out=ref)
+        assert torch.equal(out, ref)
+    assert pipe.h2d_bytes == hA.nbytes() + hBs[0].nbytes()
