@@ -55,7 +55,7 @@ constexpr int kRbkSlots = 3;
 #endif
 constexpr int kTtvLpl = SPX_TTV_LPL;
 
-template <typename T, int LPL>
+template <typename T, int LPL, bool CSMEM>
 __global__ void __launch_bounds__(kTtvWarps * 32, SPX_TTV_MINB) ttv_rbk_kernel(const int32_t* __restrict__ crd0,
                                                       const int32_t* __restrict__ pos1,
                                                       const int32_t* __restrict__ crd1,
@@ -63,8 +63,7 @@ __global__ void __launch_bounds__(kTtvWarps * 32, SPX_TTV_MINB) ttv_rbk_kernel(c
                                                       const int32_t* __restrict__ crd2,
                                                       const T* __restrict__ vals, const T* __restrict__ c,
                                                       T* __restrict__ A, int64_t S, int64_t F, int64_t J,
-                                                      int64_t K, int64_t FW, int64_t ngroups, int c_in_smem,
-                                                      int nnz) {
+                                                      int64_t K, int64_t FW, int64_t ngroups, int nnz) {
   static_assert(LPL % 4 == 0 && LPL <= 32, "whole int4 coordinate vectors per lane");
   constexpr int STEP = 32 * LPL;                       // leaves per warp step
   constexpr int SLOT = STEP * (4 + (int)sizeof(T));    // coordinates then values
@@ -73,7 +72,7 @@ __global__ void __launch_bounds__(kTtvWarps * 32, SPX_TTV_MINB) ttv_rbk_kernel(c
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   T* sc = reinterpret_cast<T*>(smem_raw + (size_t)nw * kRbkSlots * SLOT);
-  if (c_in_smem) {
+  if (CSMEM) {
     for (int64_t k = threadIdx.x; k < K; k += blockDim.x) sc[k] = __ldg(c + k);
     __syncthreads();
   }
@@ -157,10 +156,15 @@ __global__ void __launch_bounds__(kTtvWarps * 32, SPX_TTV_MINB) ttv_rbk_kernel(c
         for (int j = 0; j < LPL; ++j) v[j] = reinterpret_cast<const T*>(slot + STEP * 4)[LPL * lane + j];
         __syncwarp();  // the slot is refilled two steps later
         T x[LPL];
+        if (p >= q0 && p + STEP <= q1) {  // interior step (warp-uniform): no position masks
 #pragma unroll
-        for (int j = 0; j < LPL; ++j) {
-          const int pp = p + LPL * lane + j;
-          x[j] = (pp >= q0 && pp < q1) ? v[j] * (c_in_smem ? sc[kk[j]] : __ldg(c + kk[j])) : T(0);
+          for (int j = 0; j < LPL; ++j) x[j] = v[j] * (CSMEM ? sc[kk[j]] : __ldg(c + kk[j]));
+        } else {
+#pragma unroll
+          for (int j = 0; j < LPL; ++j) {
+            const int pp = p + LPL * lane + j;
+            x[j] = (pp >= q0 && pp < q1) ? v[j] * (CSMEM ? sc[kk[j]] : __ldg(c + kk[j])) : T(0);
+          }
         }
         // fiber starts in [p, p+STEP) as a bit mask, one word per 32 positions
         const int rel = st_mine - p;
@@ -606,7 +610,7 @@ int run_ttv(const Args& a) {
   const size_t rbytes = (size_t)nw * kRbkSlots * 32 * kTtvLpl * (4 + sizeof(T));
   const int c_in_smem = cbytes + rbytes <= kSmemBudget ? 1 : 0;
   const size_t smem = rbytes + (c_in_smem ? cbytes : 0);
-  auto kern = ttv_rbk_kernel<T, kTtvLpl>;
+  auto kern = c_in_smem ? ttv_rbk_kernel<T, kTtvLpl, true> : ttv_rbk_kernel<T, kTtvLpl, false>;
   if (int e = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                          "cudaFuncSetAttribute"))
     return e;
@@ -618,7 +622,7 @@ int run_ttv(const Args& a) {
   kern<<<(unsigned)grid, (unsigned)(nw * 32), smem, a.stream>>>(c.crd0, c.pos1, c.crd1, c.pos2, c.crd2,
                                                                  static_cast<const T*>(a.vals[0]),
                                                                  static_cast<const T*>(a.vals[1]), A, c.S, c.F, J, K,
-                                                                 FW, ceil_div(c.F, FW), c_in_smem, (int)c.nnz);
+                                                                 FW, ceil_div(c.F, FW), (int)c.nnz);
   count_launch();
   return check_cuda(cudaGetLastError(), "ttv_rbk_kernel");
 }
