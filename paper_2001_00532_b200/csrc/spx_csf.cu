@@ -206,15 +206,14 @@ __global__ void __launch_bounds__(kTtvWarps * 32, SPX_TTV_MINB) ttv_rbk_kernel(c
         // segmented inclusive scan of the partial leaving each lane; the
         // step's carry enters at lane 0
         T vs = seen ? run : run + (lane == 0 ? carry : T(0));
-        bool fl = seen || lane == 0;
+        // segment heads are the lanes that saw a start (and lane 0); a lane
+        // sums the lanes from its head on, so only values are shuffled
+        const unsigned heads = __ballot_sync(kFull, seen || lane == 0);
+        const int seg = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
           const T y = __shfl_up_sync(kFull, vs, o);
-          const bool fy = __shfl_up_sync(kFull, fl, o);
-          if (lane >= o) {
-            if (!fl) vs += y;
-            fl = fl || fy;
-          }
+          if (lane - o >= seg) vs += y;
         }
         T in = __shfl_up_sync(kFull, vs, 1);  // partial arriving at my first position
         if (lane == 0) in = carry;
