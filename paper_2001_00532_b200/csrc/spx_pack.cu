@@ -117,26 +117,39 @@ int exclusive_scan(const int64_t* in, int64_t* out, int64_t n, int64_t* ws, cuda
 }
 
 // ---------------------------------------------------------------------------
-// Stable LSD radix sort of (uint64 key, uint32 idx), 8-bit digits.
+// Stable LSD radix sort of (uint64 key, uint32 idx), kRadixBits-bit digits.
 // ---------------------------------------------------------------------------
 constexpr int kSortThreads = 256;
 constexpr int kSortRounds = 16;
 constexpr int kSortTile = kSortThreads * kSortRounds;  // 4096 keys per tile
+#ifndef SPX_RADIX_BITS
+#define SPX_RADIX_BITS 10  // 40-bit cfg2 keys: 4 passes (8-bit digits: 5)
+#endif
+constexpr int kRadixBits = SPX_RADIX_BITS;
+constexpr int kBins = 1 << kRadixBits;
+constexpr uint64_t kDigitMask = (uint64_t)kBins - 1;
+constexpr int kDPT = kBins / kSortThreads;  // digits per thread in the tile scans
+static_assert(kBins % kSortThreads == 0, "whole digits per thread");
 
 __global__ void __launch_bounds__(kSortThreads) radix_hist_kernel(const uint64_t* __restrict__ keys, int64_t n,
                                                                   int shift, int64_t ntiles,
                                                                   int64_t* __restrict__ hist) {
-  __shared__ int s_hist[256];
-  s_hist[threadIdx.x] = 0;
+  __shared__ int s_hist[kBins];
+#pragma unroll
+  for (int j = 0; j < kDPT; ++j) s_hist[j * kSortThreads + threadIdx.x] = 0;
   __syncthreads();
   const int64_t base = (int64_t)blockIdx.x * kSortTile;
 #pragma unroll 4
   for (int r = 0; r < kSortRounds; ++r) {
     const int64_t i = base + (int64_t)r * kSortThreads + threadIdx.x;
-    if (i < n) atomicAdd(&s_hist[(int)((keys[i] >> shift) & 0xff)], 1);
+    if (i < n) atomicAdd(&s_hist[(int)((keys[i] >> shift) & kDigitMask)], 1);
   }
   __syncthreads();
-  hist[(int64_t)threadIdx.x * ntiles + blockIdx.x] = s_hist[threadIdx.x];  // digit-major
+#pragma unroll
+  for (int j = 0; j < kDPT; ++j) {
+    const int d = j * kSortThreads + threadIdx.x;
+    hist[(int64_t)d * ntiles + blockIdx.x] = s_hist[d];  // digit-major
+  }
 }
 
 // Stable scatter through shared memory.  Element order inside a tile is
@@ -148,7 +161,7 @@ __global__ void __launch_bounds__(kSortThreads) radix_hist_kernel(const uint64_t
 // in that order: consecutive threads store consecutive slots of one digit's
 // bucket, whole sectors instead of one scattered 8 B and 4 B store per key
 // (the previous direct scatter: 0.93 ms per pass at cfg2).
-constexpr int kScatterSmem = kSortTile * 12 + (kSortThreads / 32) * 256 * 4 + 256 * 8 + 256 * 4;
+constexpr int kScatterSmem = kSortTile * 12 + (kSortThreads / 32) * kBins * 4 + kBins * 8 + kBins * 4;
 
 __global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
     const uint64_t* __restrict__ keys, const uint32_t* __restrict__ idx, int64_t n, int shift, int64_t ntiles,
@@ -158,16 +171,19 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint64_t* s_keys = reinterpret_cast<uint64_t*>(smem_raw);
   uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_keys + kSortTile);
-  int* s_wcnt = reinterpret_cast<int*>(s_idx + kSortTile);   // [NW][256]
-  int64_t* s_gbase = reinterpret_cast<int64_t*>(s_wcnt + NW * 256);  // [256] global bucket base
-  int* s_dstart = reinterpret_cast<int*>(s_gbase + 256);      // [256] tile-local digit start
+  int* s_wcnt = reinterpret_cast<int*>(s_idx + kSortTile);        // [NW][kBins]
+  int64_t* s_gbase = reinterpret_cast<int64_t*>(s_wcnt + NW * kBins);  // [kBins] global bucket base
+  int* s_dstart = reinterpret_cast<int*>(s_gbase + kBins);          // [kBins] tile-local digit start
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
   const int64_t base = (int64_t)blockIdx.x * kSortTile;
   const int tile_n = (int)min((int64_t)kSortTile, n - base);
+  for (int j = threadIdx.x; j < NW * kBins; j += kSortThreads) s_wcnt[j] = 0;
 #pragma unroll
-  for (int w = 0; w < NW; ++w) s_wcnt[w * 256 + threadIdx.x] = 0;
-  s_gbase[threadIdx.x] = offs[(int64_t)threadIdx.x * ntiles + blockIdx.x];
+  for (int j = 0; j < kDPT; ++j) {
+    const int d = j * kSortThreads + threadIdx.x;
+    s_gbase[d] = offs[(int64_t)d * ntiles + blockIdx.x];
+  }
   __syncthreads();
   // pass 1: load, rank inside the warp
   constexpr int R = PER_WARP / 32;  // 16 rounds
@@ -180,25 +196,32 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
     const bool ok = t < tile_n;
     k[r] = ok ? keys[base + t] : 0;
     v[r] = ok ? idx[base + t] : 0;
-    const int d = ok ? (int)((k[r] >> shift) & 0xff) : 256;  // 256: no digit
+    const int d = ok ? (int)((k[r] >> shift) & kDigitMask) : kBins;  // kBins: no digit
     const unsigned peers = __match_any_sync(kFull, d);
     const int before = __popc(peers & lt);
     int cnt = 0;
-    if (ok) cnt = s_wcnt[warp * 256 + d];
+    if (ok) cnt = s_wcnt[warp * kBins + d];
     rk[r] = cnt + before;
     __syncwarp();
-    if (ok && before == 0) s_wcnt[warp * 256 + d] = cnt + __popc(peers);
+    if (ok && before == 0) s_wcnt[warp * kBins + d] = cnt + __popc(peers);
     __syncwarp();
   }
   __syncthreads();
-  // (digit, warp) counts -> tile-local positions: digit d = this thread
+  // (digit, warp) counts -> tile-local positions; thread t owns digits
+  // [t*kDPT, t*kDPT + kDPT)
   {
-    const int d = threadIdx.x;
-    int tot = 0;
+    int tot[kDPT];
+    int mine = 0;
 #pragma unroll
-    for (int w = 0; w < NW; ++w) tot += s_wcnt[w * 256 + d];
-    // block exclusive scan of tot over the 256 digits
-    int x = tot;
+    for (int j = 0; j < kDPT; ++j) {
+      const int d = threadIdx.x * kDPT + j;
+      tot[j] = 0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) tot[j] += s_wcnt[w * kBins + d];
+      mine += tot[j];
+    }
+    // block exclusive scan of the per-thread sums
+    int x = mine;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int y = __shfl_up_sync(kFull, x, o);
@@ -210,14 +233,19 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
     int wpre = 0;
 #pragma unroll
     for (int w = 0; w < NW; ++w) wpre += (w < warp) ? s_wsum[w] : 0;
-    const int start = wpre + x - tot;
-    s_dstart[d] = start;
-    int acc = start;
+    int start = wpre + x - mine;
 #pragma unroll
-    for (int w = 0; w < NW; ++w) {
-      const int c = s_wcnt[w * 256 + d];
-      s_wcnt[w * 256 + d] = acc;
-      acc += c;
+    for (int j = 0; j < kDPT; ++j) {
+      const int d = threadIdx.x * kDPT + j;
+      s_dstart[d] = start;
+      int acc = start;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        const int c = s_wcnt[w * kBins + d];
+        s_wcnt[w * kBins + d] = acc;
+        acc += c;
+      }
+      start += tot[j];
     }
   }
   __syncthreads();
@@ -226,8 +254,8 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
   for (int r = 0; r < R; ++r) {
     const int t = warp * PER_WARP + r * 32 + lane;
     if (t < tile_n) {
-      const int d = (int)((k[r] >> shift) & 0xff);
-      const int pos = s_wcnt[warp * 256 + d] + rk[r];
+      const int d = (int)((k[r] >> shift) & kDigitMask);
+      const int pos = s_wcnt[warp * kBins + d] + rk[r];
       s_keys[pos] = k[r];
       s_idx[pos] = v[r];
     }
@@ -236,7 +264,7 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
   // pass 3: write out in sorted order (runs of one digit are contiguous)
   for (int t = threadIdx.x; t < tile_n; t += kSortThreads) {
     const uint64_t kk = s_keys[t];
-    const int d = (int)((kk >> shift) & 0xff);
+    const int d = (int)((kk >> shift) & kDigitMask);
     const int64_t dst = s_gbase[d] + (t - s_dstart[d]);
     keys_out[dst] = kk;
     idx_out[dst] = s_idx[t];
@@ -264,9 +292,9 @@ PackLayout pack_layout(int64_t n) {
   L.idx2 = take(nn * 4);
   L.flags = take(nn * 8);
   L.ex = take(nn * 8);
-  L.hist = take((size_t)256 * ntiles * 8);
-  L.offs = take((size_t)256 * ntiles * 8);
-  L.scan = take(scan_ws_bytes((int64_t)nn > 256 * ntiles ? (int64_t)nn : 256 * ntiles));
+  L.hist = take((size_t)kBins * ntiles * 8);
+  L.offs = take((size_t)kBins * ntiles * 8);
+  L.scan = take(scan_ws_bytes((int64_t)nn > kBins * ntiles ? (int64_t)nn : kBins * ntiles));
   L.total = off;
   return L;
 }
@@ -460,11 +488,11 @@ int spx_pack_sort_strided(const int32_t* const* coords_host, int64_t coord_strid
                                               kScatterSmem),
                          "cudaFuncSetAttribute"))
     return e;
-  for (int shift = 0; shift < bits; shift += 8) {
+  for (int shift = 0; shift < bits; shift += kRadixBits) {
     radix_hist_kernel<<<(unsigned)ntiles, kSortThreads, 0, s>>>(keys, n, shift, ntiles, hist);
     count_launch();
     if (int e = check_cuda(cudaGetLastError(), "radix_hist_kernel")) return e;
-    if (int e = exclusive_scan(hist, offs, 256 * ntiles, scan_ws, s)) return e;
+    if (int e = exclusive_scan(hist, offs, (int64_t)kBins * ntiles, scan_ws, s)) return e;
     radix_scatter_kernel<<<(unsigned)ntiles, kSortThreads, kScatterSmem, s>>>(keys, idx, n, shift, ntiles, offs,
                                                                               keys2, idx2);
     count_launch();
