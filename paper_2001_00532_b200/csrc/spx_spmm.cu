@@ -523,7 +523,14 @@ int run_spmm(int kid, const Args& a, const SpmmGeom& g) {
   int64_t nw = a.params[1] > 0 ? a.params[1] : (R < 8 ? R : 8);
   if (nw > kMaxWarps) nw = kMaxWarps;
   dim3 grid((unsigned)ceil_div(M, R), (unsigned)g.npanels);
-  constexpr int UR = U > 4 ? 4 : U;  // B rows in flight per warp (register budget)
+#ifndef SPX_SPMM_ROW_UR
+#define SPX_SPMM_ROW_UR 8
+#endif
+  // B rows in flight per warp: the register budget holds SPX_SPMM_ROW_UR
+  // 4-float (16 B per lane) rows; the heaviest row (one warp, by the schedule) is
+  // latency-bound, so deeper is better while nothing spills
+  constexpr int UR_MAX = SPX_SPMM_ROW_UR * 16 / (VPL * (int)sizeof(T));  // 32-bit registers per row: VPL*sizeof/4
+  constexpr int UR = UR_MAX < 1 ? 1 : (UR_MAX > 16 ? 16 : UR_MAX);
   spmm_row_kernel<T, VPL, CONTIG, UR><<<grid, (unsigned)(nw * 32), (size_t)nw * LeafRing<T, 4>::kBytes, a.stream>>>(
       pos, crd, vals, B, C, M, N, R);
   count_launch();
