@@ -17,6 +17,12 @@
 #include "spx_common.cuh"
 
 // tuning knob: 3 CTAs/SM forces 40 registers and spills 48-280 B per thread
+#ifndef SPX_SDDMM_ROW_MINB
+#define SPX_SDDMM_ROW_MINB 1  // the heaviest row is latency-bound: more rows in flight beat occupancy
+#endif
+#ifndef SPX_SDDMM_ROW_UR
+#define SPX_SDDMM_ROW_UR 4   // cfg3 K10: 7.8 ms (2 rows, 2 CTAs/SM) -> 5.7 ms
+#endif
 #ifndef SPX_SDDMM_MINB
 #define SPX_SDDMM_MINB 2
 #endif
@@ -149,7 +155,7 @@ __global__ void __launch_bounds__(kMaxThreads, SPX_SDDMM_MINB) sddmm_nnz_kernel(
 // (C row loaded once per row, (column, value) pairs on the warp's LeafRing,
 // eight dot products per transpose_reduce8, coalesced stores).
 template <typename T, int VPL, bool CONTIG, int U>
-__global__ void __launch_bounds__(kMaxThreads, 2) sddmm_row_kernel(const int32_t* __restrict__ pos,
+__global__ void __launch_bounds__(kMaxThreads, SPX_SDDMM_ROW_MINB) sddmm_row_kernel(const int32_t* __restrict__ pos,
                                                             const int32_t* __restrict__ crd,
                                                             const T* __restrict__ vals, const T* __restrict__ Cm,
                                                             const T* __restrict__ Dm, T* __restrict__ out, int64_t M,
@@ -247,7 +253,7 @@ int run_sddmm(int kid, const Args& a) {
   const int64_t R = a.params[0] > 0 ? a.params[0] : 8;
   int64_t nw = a.params[1] > 0 ? a.params[1] : (R < 8 ? R : 8);
   if (nw > kMaxWarps) nw = kMaxWarps;
-  constexpr int UR = VPL * (int)sizeof(T) >= 32 ? 2 : 4;  // D rows in flight per warp
+  constexpr int UR = VPL * (int)sizeof(T) >= 32 ? SPX_SDDMM_ROW_UR : 4;  // D rows in flight per warp
   sddmm_row_kernel<T, VPL, CONTIG, UR><<<(unsigned)ceil_div(M, R), (unsigned)(nw * 32),
                                          (size_t)nw * LeafRing<T, 4>::kBytes, a.stream>>>(pos, crd, vals, Cm, Dm, out,
                                                                                           M, N, K, R, dense);
