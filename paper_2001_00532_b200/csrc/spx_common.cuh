@@ -206,6 +206,44 @@ struct LeafRing {
   __device__ __forceinline__ void release() { __syncwarp(); }
 };
 
+
+// 16 B / 8 B vectors <-> T elements through register bit casts (no type-punned
+// stores into the per-lane arrays, which force them into local memory for fp64)
+template <typename T>
+__device__ __forceinline__ void unpack16(T* d, const float4& q) {
+  if constexpr (sizeof(T) == 4) {
+    d[0] = q.x; d[1] = q.y; d[2] = q.z; d[3] = q.w;
+  } else {
+    d[0] = __hiloint2double(__float_as_int(q.y), __float_as_int(q.x));
+    d[1] = __hiloint2double(__float_as_int(q.w), __float_as_int(q.z));
+  }
+}
+template <typename T>
+__device__ __forceinline__ float4 pack16(const T* s) {
+  if constexpr (sizeof(T) == 4) {
+    return make_float4(s[0], s[1], s[2], s[3]);
+  } else {
+    return make_float4(__int_as_float(__double2loint(s[0])), __int_as_float(__double2hiint(s[0])),
+                       __int_as_float(__double2loint(s[1])), __int_as_float(__double2hiint(s[1])));
+  }
+}
+template <typename T>
+__device__ __forceinline__ void unpack8(T* d, const float2& q) {
+  if constexpr (sizeof(T) == 4) {
+    d[0] = q.x; d[1] = q.y;
+  } else {
+    d[0] = __hiloint2double(__float_as_int(q.y), __float_as_int(q.x));
+  }
+}
+template <typename T>
+__device__ __forceinline__ float2 pack8(const T* s) {
+  if constexpr (sizeof(T) == 4) {
+    return make_float2(s[0], s[1]);
+  } else {
+    return make_float2(__int_as_float(__double2loint(s[0])), __int_as_float(__double2hiint(s[0])));
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Per-lane row fragments: a lane owns VPL values of a dense row.
 // CONTIG: lane owns columns [lane*VPL, lane*VPL+VPL) -> vector loads.
@@ -229,13 +267,13 @@ struct Frag {
 #pragma unroll
         for (int c = 0; c < BYTES / 16; ++c) {
           float4 q = __ldg(reinterpret_cast<const float4*>(p) + c);
-          *reinterpret_cast<float4*>(&v[c * (16 / sizeof(T))]) = q;
+          unpack16(&v[c * (16 / sizeof(T))], q);
         }
       } else if constexpr (BYTES % 8 == 0) {
 #pragma unroll
         for (int c = 0; c < BYTES / 8; ++c) {
           float2 q = __ldg(reinterpret_cast<const float2*>(p) + c);
-          *reinterpret_cast<float2*>(&v[c * (8 / sizeof(T))]) = q;
+          unpack8(&v[c * (8 / sizeof(T))], q);
         }
       } else {
 #pragma unroll
@@ -258,13 +296,13 @@ struct Frag {
 #pragma unroll
       for (int c = 0; c < BYTES / 16; ++c) {
         float4 q = __ldg(reinterpret_cast<const float4*>(p) + c);
-        *reinterpret_cast<float4*>(&v[c * (16 / sizeof(T))]) = q;
+        unpack16(&v[c * (16 / sizeof(T))], q);
       }
     } else if constexpr (BYTES % 8 == 0) {
 #pragma unroll
       for (int c = 0; c < BYTES / 8; ++c) {
         float2 q = __ldg(reinterpret_cast<const float2*>(p) + c);
-        *reinterpret_cast<float2*>(&v[c * (8 / sizeof(T))]) = q;
+        unpack8(&v[c * (8 / sizeof(T))], q);
       }
     } else {
 #pragma unroll
@@ -279,7 +317,7 @@ struct Frag {
 #pragma unroll
       for (int c = 0; c < BYTES / 16; ++c) {
         float4 q = ld_f4_hint(reinterpret_cast<const float4*>(p) + c, pol);
-        *reinterpret_cast<float4*>(&v[c * (16 / sizeof(T))]) = q;
+        unpack16(&v[c * (16 / sizeof(T))], q);
       }
     } else {
       load_ptr(p);
@@ -294,7 +332,7 @@ struct Frag {
 #pragma unroll
       for (int c = 0; c < BYTES / 16; ++c) {
         float4 q = ld_f4_hint(reinterpret_cast<const float4*>(p) + c, pol);
-        *reinterpret_cast<float4*>(&v[c * (16 / sizeof(T))]) = q;
+        unpack16(&v[c * (16 / sizeof(T))], q);
       }
     } else {
       load(row, lane, ncols);
@@ -307,7 +345,7 @@ struct Frag {
       T* p = row + lane * VPL;
 #pragma unroll
       for (int c = 0; c < BYTES / 16; ++c)
-        st_f4_hint(reinterpret_cast<float4*>(p) + c, *reinterpret_cast<const float4*>(&v[c * (16 / sizeof(T))]),
+        st_f4_hint(reinterpret_cast<float4*>(p) + c, pack16(&v[c * (16 / sizeof(T))]),
                    pol);
     } else {
       store(row, lane, ncols);
@@ -322,12 +360,12 @@ struct Frag {
 #pragma unroll
         for (int c = 0; c < BYTES / 16; ++c)
           __stcs(reinterpret_cast<float4*>(p) + c,
-                 *reinterpret_cast<const float4*>(&v[c * (16 / sizeof(T))]));
+                 pack16(&v[c * (16 / sizeof(T))]));
       } else if constexpr (BYTES % 8 == 0) {
 #pragma unroll
         for (int c = 0; c < BYTES / 8; ++c)
           __stcs(reinterpret_cast<float2*>(p) + c,
-                 *reinterpret_cast<const float2*>(&v[c * (8 / sizeof(T))]));
+                 pack8(&v[c * (8 / sizeof(T))]));
       } else {
 #pragma unroll
         for (int i = 0; i < VPL; ++i) __stcs(p + i, v[i]);

@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(kMaxThreads, RING == 0 ? SPX_SPMM_MINB : 1) sp
             vv[u] = __shfl_sync(kFull, b0.v, j * GS + u);
             const float4* sp = reinterpret_cast<const float4*>(ring_lane + ((j * GS + u) % RING) * PW);
 #pragma unroll
-            for (int k = 0; k < LB / 16; ++k) *reinterpret_cast<float4*>(&bv[u].v[k * (16 / sizeof(T))]) = sp[k];
+            for (int k = 0; k < LB / 16; ++k) unpack16(&bv[u].v[k * (16 / sizeof(T))], sp[k]);
           }
           if (cnt == GS && gbase + GS <= rend) {
 #pragma unroll
@@ -350,8 +350,11 @@ __global__ void carry_fixup_kernel(const int32_t* __restrict__ carry_row, const 
 // broadcasts; B rows are gathered U at a time into registers.  A row longer
 // than the ring keeps streaming, so one warp on a long row still has ~U rows
 // of B and three batches of A in flight.
+#ifndef SPX_SPMM_ROW_MINB
+#define SPX_SPMM_ROW_MINB 1  // K5: the heaviest row is latency-bound; 16 rows in flight beat occupancy
+#endif
 template <typename T, int VPL, bool CONTIG, int U>
-__global__ void __launch_bounds__(kMaxThreads, 2) spmm_row_kernel(
+__global__ void __launch_bounds__(kMaxThreads, SPX_SPMM_ROW_MINB) spmm_row_kernel(
     const int32_t* __restrict__ pos, const int32_t* __restrict__ crd, const T* __restrict__ vals,
     const T* __restrict__ B, T* __restrict__ C, int64_t M, int64_t N, int64_t R) {
   using F = Frag<T, VPL, CONTIG>;
@@ -524,7 +527,7 @@ int run_spmm(int kid, const Args& a, const SpmmGeom& g) {
   if (nw > kMaxWarps) nw = kMaxWarps;
   dim3 grid((unsigned)ceil_div(M, R), (unsigned)g.npanels);
 #ifndef SPX_SPMM_ROW_UR
-#define SPX_SPMM_ROW_UR 8
+#define SPX_SPMM_ROW_UR 16
 #endif
   // B rows in flight per warp: the register budget holds SPX_SPMM_ROW_UR
   // 4-float (16 B per lane) rows; the heaviest row (one warp, by the schedule) is

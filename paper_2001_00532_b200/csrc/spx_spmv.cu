@@ -154,7 +154,7 @@ __device__ __forceinline__ void load_thread_chunk(const int32_t* __restrict__ cr
 #pragma unroll
       for (int k = 0; k < TPT / kPer; ++k) {
         const float4 q = __ldcs(reinterpret_cast<const float4*>(vals + a) + k);
-        *reinterpret_cast<float4*>(&vv[kPer * k]) = q;
+        unpack16(&vv[kPer * k], q);
       }
     }
   } else {
