@@ -256,6 +256,12 @@ constexpr int kMttkrpThreads = SPX_MTTKRP_THREADS;
 #ifndef SPX_MTTKRP_G
 #define SPX_MTTKRP_G 4
 #endif
+#ifndef SPX_MTTKRP_SLICE_G
+#define SPX_MTTKRP_SLICE_G 8
+#endif
+#ifndef SPX_MTTKRP_SLICE_MINB
+#define SPX_MTTKRP_SLICE_MINB 1
+#endif
 #ifndef SPX_MTTKRP_MINB
 #define SPX_MTTKRP_MINB 2
 #endif
@@ -408,7 +414,9 @@ __device__ __forceinline__ void mttkrp_walk(const MttkrpCtx<T, VPL, CONTIG>& c, 
                                             int q0, int q1, int f, int s) {
   if constexpr (std::is_same<T, float>::value && VPL == 1 && CONTIG) {
     if (c.R == 32) {
-      mttkrp_walk_quad<OWNED, SPX_MTTKRP_G>(c, ring_base, lane, q0, q1, f, s);
+      // slice-split (OWNED): one warp walks a whole slice, so the largest slice is
+      // latency-bound and gets twice the leaves in flight (the kernel runs 1 CTA/SM)
+      mttkrp_walk_quad<OWNED, OWNED ? SPX_MTTKRP_SLICE_G : SPX_MTTKRP_G>(c, ring_base, lane, q0, q1, f, s);
       return;
     }
   }
@@ -549,7 +557,7 @@ __global__ void __launch_bounds__(kMttkrpThreads, SPX_MTTKRP_MINB) mttkrp_nnz_ke
 // K9: slice-split (A.5 shape) -- one warp per slice, plain stores;
 // persistent CTAs walk the slices round-robin.
 template <typename T, int VPL, bool CONTIG>
-__global__ void __launch_bounds__(kMttkrpThreads, 2) mttkrp_slice_kernel(
+__global__ void __launch_bounds__(kMttkrpThreads, SPX_MTTKRP_SLICE_MINB) mttkrp_slice_kernel(
     const int32_t* __restrict__ crd0, const int32_t* __restrict__ pos1, const int32_t* __restrict__ crd1,
     const int32_t* __restrict__ pos2, const int32_t* __restrict__ crd2, const T* __restrict__ vals,
     const T* __restrict__ Cm, const T* __restrict__ Dm, T* __restrict__ A, int64_t S, int64_t F, int64_t R) {
