@@ -24,8 +24,25 @@ namespace {
 
 constexpr int kPosCache = 4096;  // ints of pos staged per CTA
 
+// Row kernels are bound by their heaviest row (one thread / one warp by the
+// schedule), which is a latency chain: the loads in flight per step are
+// tuning knobs (SPX_SPMV_ROW_STEP positions per thread, SPX_SPMV_WARP_STEPS
+// 32-position steps per warp) traded against occupancy (..._MINB).
+#ifndef SPX_SPMV_ROW_STEP
+#define SPX_SPMV_ROW_STEP 32  // cfg5 A7 15.1 -> 9.2 ms (one CTA/SM)
+#endif
+#ifndef SPX_SPMV_ROW_MINB
+#define SPX_SPMV_ROW_MINB 1
+#endif
+#ifndef SPX_SPMV_WARP_STEPS
+#define SPX_SPMV_WARP_STEPS 8  // cfg5 A8 2.29 -> 1.70 ms; 16 steps at 1 CTA/SM: 2.47
+#endif
+#ifndef SPX_SPMV_WARP_MINB
+#define SPX_SPMV_WARP_MINB 2
+#endif
+
 template <typename T>
-__global__ void __launch_bounds__(kMaxThreads, 2) spmv_row_kernel(const int32_t* __restrict__ pos,
+__global__ void __launch_bounds__(kMaxThreads, SPX_SPMV_ROW_MINB) spmv_row_kernel(const int32_t* __restrict__ pos,
                                                         const int32_t* __restrict__ crd,
                                                         const T* __restrict__ vals, const T* __restrict__ x,
                                                         T* __restrict__ y, int64_t M, int64_t R) {
@@ -34,22 +51,23 @@ __global__ void __launch_bounds__(kMaxThreads, 2) spmv_row_kernel(const int32_t*
     const int64_t i = lo + t;
     if (i >= M) return;
     const int a = __ldg(pos + i), e = __ldg(pos + i + 1);
-    // eight positions' loads in flight per step (a long row is one thread's
+    // STEP positions' loads in flight per step (a long row is one thread's
     // serial dependency chain otherwise); sequential fold order kept
+    constexpr int STEP = SPX_SPMV_ROW_STEP;
     T acc = T(0);
     int p = a;
-    for (; p + 8 <= e; p += 8) {
-      int c[8];
-      T v[8], xv[8];
+    for (; p + STEP <= e; p += STEP) {
+      int c[STEP];
+      T v[STEP], xv[STEP];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
+      for (int k = 0; k < STEP; ++k) {
         c[k] = __ldcs(crd + p + k);
         v[k] = __ldcs(vals + p + k);
       }
 #pragma unroll
-      for (int k = 0; k < 8; ++k) xv[k] = __ldg(x + c[k]);
+      for (int k = 0; k < STEP; ++k) xv[k] = __ldg(x + c[k]);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) acc += v[k] * xv[k];
+      for (int k = 0; k < STEP; ++k) acc += v[k] * xv[k];
     }
     for (; p < e; ++p) acc += __ldcs(vals + p) * __ldg(x + __ldcs(crd + p));
     __stcs(y + i, acc);
@@ -57,7 +75,7 @@ __global__ void __launch_bounds__(kMaxThreads, 2) spmv_row_kernel(const int32_t*
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kMaxThreads, 2) spmv_warp_kernel(const int32_t* __restrict__ pos,
+__global__ void __launch_bounds__(kMaxThreads, SPX_SPMV_WARP_MINB) spmv_warp_kernel(const int32_t* __restrict__ pos,
                                                          const int32_t* __restrict__ crd,
                                                          const T* __restrict__ vals, const T* __restrict__ x,
                                                          T* __restrict__ y, int64_t M, int64_t R) {
@@ -71,22 +89,23 @@ __global__ void __launch_bounds__(kMaxThreads, 2) spmv_warp_kernel(const int32_t
     const int64_t i = lo + br;
     if (i >= M) break;
     const int a = __ldg(pos + i), e = __ldg(pos + i + 1);
-    // lanes stride the row (thread_nz x thread); four 32-position steps'
+    // lanes stride the row (thread_nz x thread); S 32-position steps'
     // loads are in flight at once, then the Temporary fold
+    constexpr int S = SPX_SPMV_WARP_STEPS;
     T acc = T(0);
     int p = a + lane;
-    for (; p + 96 < e; p += 128) {
-      int c[4];
-      T v[4], xv[4];
+    for (; p + 32 * (S - 1) < e; p += 32 * S) {
+      int c[S];
+      T v[S], xv[S];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < S; ++k) {
         c[k] = __ldcs(crd + p + 32 * k);
         v[k] = __ldcs(vals + p + 32 * k);
       }
 #pragma unroll
-      for (int k = 0; k < 4; ++k) xv[k] = __ldg(x + c[k]);
+      for (int k = 0; k < S; ++k) xv[k] = __ldg(x + c[k]);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) acc += v[k] * xv[k];
+      for (int k = 0; k < S; ++k) acc += v[k] * xv[k];
     }
     for (; p < e; p += 32) acc += __ldcs(vals + p) * __ldg(x + __ldcs(crd + p));
 #pragma unroll
