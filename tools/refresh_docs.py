@@ -118,6 +118,11 @@ def baseline_table(s: str) -> str:
                f"The bench line itself ({b['ms_per_step']:.3f} ms, {b['value']:,.0f} GFLOP/s)", s)
     s = re.sub(r"1 s load at the power cap \([0-9]+ of [0-9]+ MHz",
                f"1 s load at the power cap ({b['clocks']['sm_mhz']:.0f} of {b['clocks']['sm_max_mhz']:.0f} MHz", s)
+    sh = [json.loads(l) for l in open(PROF / "r01_shard_scaling.jsonl")]
+    sp = {r["cfg"]: r["speedup_vs_1"] for r in sh if r["gpus"] == 8}
+    s = re.sub(r"r01_shard_scaling.jsonl`\): [0-9.]+× for cfg2 SpMM and [0-9.]+× for cfg5 SpMV at\n  8 GPUs, [0-9.]+× for cfg4 MTTKRP",
+               f"r01_shard_scaling.jsonl`): {sp[2]:.2f}× for cfg2 SpMM and {sp[5]:.2f}× for cfg5 SpMV at\n"
+               f"  8 GPUs, {sp[4]:.2f}× for cfg4 MTTKRP", s)
     return s
 
 
