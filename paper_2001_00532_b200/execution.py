@@ -88,6 +88,21 @@ class Executor:
         )
         _lib.check(st, f"spx_launch[{self.program.kernel}]")
 
+    def capture(self, repeat: int = 1) -> "torch.cuda.CUDAGraph":
+        """Capture `repeat` launches into a CUDA graph; `g.replay()` then
+        costs one graph launch on the host instead of the launch sequence
+        (chunk table, kernel, fix-up / memset) per step -- the form for
+        launch-bound loops: small operands, iterative solvers calling the
+        same SpMV.  Operand and output buffers are bound at capture, so
+        refill them in place between replays."""
+        self.launch()  # first launch outside capture: module load, smem attributes
+        torch.cuda.synchronize(self.out.device)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(repeat):
+                self.launch()
+        return g
+
     def stats(self) -> "ExecStats":
         return ExecStats(self.program, self.plan, self.sparse, self.dims_map)
 
