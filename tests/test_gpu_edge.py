@@ -44,6 +44,7 @@ def _matrices():
         "single_row": np.array([1500]),
         "alternating": np.tile([0, 17, 0, 3, 40], 60),
         "powerlaw": np.minimum(rng.zipf(1.6, 800), 2500),
+        "staircase": np.arange(0, 140),  # every row length 0..139: all tails of the 8/16/32-wide steps
     }
     return {k: _csr_from_lengths(v, K, 1) + (K,) for k, v in out.items()}
 
