@@ -109,6 +109,7 @@ extern "C" {
 #define SPX_K_MTTKRP_NNZ 8
 #define SPX_K_MTTKRP_SLICE 9
 #define SPX_K_SDDMM_ROW 10
+#define SPX_K_TTV_NNZ 11
 
 typedef struct spx_plan {
   int32_t kernel_id;

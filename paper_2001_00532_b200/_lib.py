@@ -38,6 +38,7 @@ K_TTV_FIBER = 7
 K_MTTKRP_NNZ = 8
 K_MTTKRP_SLICE = 9
 K_SDDMM_ROW = 10
+K_TTV_NNZ = 11
 
 KERNEL_NAMES = {
     K_SPMV_ROW: "spmv_row",
@@ -50,6 +51,7 @@ KERNEL_NAMES = {
     K_MTTKRP_NNZ: "mttkrp_nnz",
     K_MTTKRP_SLICE: "mttkrp_slice",
     K_SDDMM_ROW: "sddmm_row",
+    K_TTV_NNZ: "ttv_nnz",
 }
 
 # every symbol include/spx.h declares (checked by tests)

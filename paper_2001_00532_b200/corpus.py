@@ -163,6 +163,18 @@ split(fpos, block, fpos1, {FIBERS_PER_TB})
 split(fpos1, warp, fiber, {FIBERS_PER_WARP})
 parallelize(block, GPUBlock, IgnoreRaces)
 parallelize(warp, GPUWarp, IgnoreRaces)""", {"FIBERS_PER_TB": 256, "FIBERS_PER_WARP": 32}, "ttv_fiber"),
+    Entry("K11", "nnz-split TTV (the A.2 shape over the leaves of fuse(i, fuse(j, k)))", TTV, F_TTV,
+          """fuse(j, k, jk)
+fuse(i, jk, f)
+pos(f, fpos, B(i,j,k))
+split(fpos, block, fpos1, {NNZ_PER_TB})
+split(fpos1, warp, fpos2, {NNZ_PER_WARP})
+split(fpos2, thread, thread_nz, {NNZ_PER_THREAD})
+reorder(block, warp, thread, thread_nz)
+parallelize(block, GPUBlock, IgnoreRaces)
+parallelize(warp, GPUWarp, IgnoreRaces)
+parallelize(thread, GPUThread, Atomics)""",
+          {"NNZ_PER_TB": 2048, "NNZ_PER_WARP": 256, "NNZ_PER_THREAD": 8}, "ttv_nnz"),
     Entry("K9", "slice-split MTTKRP on GPU (row a20 K9, A.5 shape)", MTTKRP, F_MTTKRP,
           """pos(i, ipos, B(i,k,l))
 split(ipos, block, warp, {SLICES_PER_TB})

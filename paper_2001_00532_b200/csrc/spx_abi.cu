@@ -38,6 +38,7 @@ bool family_of(int kid, Family* f) {
       *f = {3, {2, 2, 2}, 1, launch_sddmm};
       return true;
     case SPX_K_TTV_FIBER:
+    case SPX_K_TTV_NNZ:
       *f = {2, {3, 1, 0}, 3, launch_csf};
       return true;
     case SPX_K_MTTKRP_NNZ:
@@ -180,7 +181,8 @@ size_t spx_workspace_size(const spx_plan* plan, const int32_t* dims) {
   switch (plan->kernel_id) {
     case SPX_K_SPMV_NNZ: return ws_spmv(plan->kernel_id, a);
     case SPX_K_SPMM_NNZ: return ws_spmm(plan->kernel_id, a);
-    case SPX_K_MTTKRP_NNZ: return ws_csf(plan->kernel_id, a);
+    case SPX_K_MTTKRP_NNZ:
+    case SPX_K_TTV_NNZ: return ws_csf(plan->kernel_id, a);
     case SPX_K_SDDMM_NNZ: return ws_sddmm(plan->kernel_id, a);
     default: return 0;
   }

@@ -696,9 +696,78 @@ int dispatch_mttkrp(int kid, const Args& a, int64_t R) {
   return fail(SPX_E_UNSUPPORTED, "no MTTKRP instantiation");
 }
 
+// K11 TTV nnz-split: pos over the leaves of the fused (i,j,k) space split
+// into NNZ_PER_TB / NNZ_PER_WARP / NNZ_PER_THREAD chunks -- the A.2 SpMV
+// shape applied to TTV.  The fibers are segments of the leaf array (pos2),
+// so the Atomics segment sum of the nnz-split SpMV produces the per-fiber
+// sums into a workspace vector, and one pass scatters them to A[i, j].
+template <typename T>
+__global__ void ttv_scatter_kernel(const int32_t* __restrict__ crd0, const int32_t* __restrict__ pos1,
+                                   const int32_t* __restrict__ crd1, const T* __restrict__ fsum, T* __restrict__ A,
+                                   int64_t S, int64_t F, int64_t J) {
+  const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= F) return;
+  int64_t lo = 0, hi = S;  // the slice of fiber f: largest s with pos1[s] <= f (SearchSegment)
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (__ldg(pos1 + mid) <= f) lo = mid;
+    else hi = mid;
+  }
+  A[(int64_t)__ldg(crd0 + lo) * J + __ldg(crd1 + f)] = fsum[f];
+}
+
+struct TtvNnzLayout {
+  size_t fsum, first, total;
+  int64_t nslots;
+};
+TtvNnzLayout ttv_nnz_layout(const Args& a) {
+  const int64_t F = a.level_sizes[1], nnz = a.level_sizes[2];
+  const int64_t TB = a.params[0] > 0 ? a.params[0] : 1;
+  const int64_t W = a.params[1] > 0 ? a.params[1] : TB;
+  const size_t es = a.dtype == SPX_F32 ? 4 : 8;
+  TtvNnzLayout L;
+  L.nslots = (nnz == 0 ? 1 : ceil_div(nnz, TB)) * (TB / W > 0 ? TB / W : 1);
+  L.fsum = 0;
+  L.first = ((size_t)(F > 0 ? F : 1) * es + 255) & ~(size_t)255;
+  L.total = L.first + (size_t)(L.nslots + 1) * sizeof(int32_t);
+  return L;
+}
+
+template <typename T>
+int run_ttv_nnz(const Args& a) {
+  const Csf c = csf_of(a);
+  const int64_t I = a.dims[0][0], J = a.dims[0][1];
+  T* A = static_cast<T*>(a.out);
+  if (int e = check_cuda(cudaMemsetAsync(A, 0, (size_t)(I * J) * sizeof(T), a.stream), "memset")) return e;
+  if (c.nnz == 0) return SPX_OK;
+  const int64_t TB = a.params[0], W = a.params[1], TPT = a.params[2];
+  if (TB < 1 || W < 1 || TPT < 1 || W != 32 * TPT || TB % W != 0 || TB / TPT > kMaxThreads)
+    return fail(SPX_E_UNSUPPORTED,
+                "TTV nnz-split needs NNZ_PER_WARP == 32*NNZ_PER_THREAD and NNZ_PER_TB a multiple of "
+                "NNZ_PER_WARP with <= 512 threads (got %lld, %lld, %lld)",
+                (long long)TB, (long long)W, (long long)TPT);
+  const TtvNnzLayout L = ttv_nnz_layout(a);
+  if (!a.ws || a.ws_bytes < L.total) return fail(SPX_E_WORKSPACE, "workspace %zu < %zu bytes", a.ws_bytes, L.total);
+  T* fsum = reinterpret_cast<T*>(static_cast<char*>(a.ws) + L.fsum);
+  int32_t* first = reinterpret_cast<int32_t*>(static_cast<char*>(a.ws) + L.first);
+  if (int e = check_cuda(cudaMemsetAsync(fsum, 0, (size_t)c.F * sizeof(T), a.stream), "memset")) return e;
+  if (int e = launch_chunk_segments(c.pos2, c.F, W, L.nslots, first, a.stream)) return e;
+  const T* vals = static_cast<const T*>(a.vals[0]);
+  const T* cv = static_cast<const T*>(a.vals[1]);
+  int e;
+  if constexpr (sizeof(T) == 4) e = segsum_atomic_f32(c.pos2, c.crd2, vals, cv, fsum, c.F, c.nnz, TB, W, TPT, first, a.stream);
+  else e = segsum_atomic_f64(c.pos2, c.crd2, vals, cv, fsum, c.F, c.nnz, TB, W, TPT, first, a.stream);
+  if (e) return e;
+  ttv_scatter_kernel<T><<<(unsigned)ceil_div(c.F, 256), 256, 0, a.stream>>>(c.crd0, c.pos1, c.crd1, fsum, A, c.S,
+                                                                          c.F, J);
+  count_launch();
+  return check_cuda(cudaGetLastError(), "ttv_scatter_kernel");
+}
+
 }  // namespace
 
 size_t ws_csf(int kid, const Args& a) {
+  if (kid == SPX_K_TTV_NNZ) return ttv_nnz_layout(a).total;
   if (kid != SPX_K_MTTKRP_NNZ) return 0;
   const int64_t nnz = a.level_sizes[2];
   const int64_t W = a.params[1] > 0 ? a.params[1] : 1;
@@ -706,10 +775,11 @@ size_t ws_csf(int kid, const Args& a) {
 }
 
 int launch_csf(int kid, const Args& a) {
-  if (kid == SPX_K_TTV_FIBER) {
+  if (kid == SPX_K_TTV_FIBER || kid == SPX_K_TTV_NNZ) {
     if (a.dims[1][0] != a.dims[0][2])
       return fail(SPX_E_ARG, "TTV: B's third dimension %lld != length of c %lld", (long long)a.dims[0][2],
                   (long long)a.dims[1][0]);
+    if (kid == SPX_K_TTV_NNZ) return a.dtype == SPX_F32 ? run_ttv_nnz<float>(a) : run_ttv_nnz<double>(a);
     return a.dtype == SPX_F32 ? run_ttv<float>(a) : run_ttv<double>(a);
   }
   const int64_t R = a.dims[1][1];

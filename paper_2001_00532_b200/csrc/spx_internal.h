@@ -66,6 +66,13 @@ inline NnzWorkspace nnz_workspace(int64_t ncta, size_t es, int64_t vals_per_cta 
 // first position it holds); chunks at or past the last position and the
 // sentinel first[nchunks] get nseg - 1.  Replaces a serial
 // binary search at the start of every CTA/warp of the nnz-split kernels.
+// the Atomics nnz-split segment sum of spx_spmv.cu (y zeroed by the caller)
+int segsum_atomic_f32(const int32_t* pos, const int32_t* crd, const float* vals, const float* x, float* y,
+                      int64_t nseg, int64_t nnz, int64_t TB, int64_t W, int64_t TPT, const int32_t* first,
+                      cudaStream_t st);
+int segsum_atomic_f64(const int32_t* pos, const int32_t* crd, const double* vals, const double* x, double* y,
+                      int64_t nseg, int64_t nnz, int64_t TB, int64_t W, int64_t TPT, const int32_t* first,
+                      cudaStream_t st);
 int launch_chunk_segments(const int32_t* pos, int64_t nseg, int64_t chunk, int64_t nchunks, int32_t* first,
                           cudaStream_t stream);
 

@@ -476,6 +476,26 @@ __global__ void spmv_fixup_kernel(const int32_t* __restrict__ carry_row, const T
   y[row] = __ldcg(y + row) + s;
 }
 
+// The Atomics nnz-split kernel over any segment structure: y[r] =
+// sum_{p in [pos[r], pos[r+1])} vals[p] * x[crd[p]] for r < nseg, with y
+// zeroed by the caller and `first` the chunk table at W granularity.  SpMV
+// (rows) and the nnz-split TTV (fibers of a CSF tensor) share it.
+template <typename T>
+int segsum_atomic(const int32_t* pos, const int32_t* crd, const T* vals, const T* x, T* y, int64_t nseg,
+                  int64_t nnz, int64_t TB, int64_t W, int64_t TPT, const int32_t* first, cudaStream_t st) {
+  const int threads = (int)(TB / TPT);
+  const unsigned g = (unsigned)(nnz == 0 ? 1 : ceil_div(nnz, TB));
+  switch (TPT) {
+    case 4: spmv_nnz_atomic_kernel<T, 4><<<g, threads, 0, st>>>(pos, crd, vals, x, y, nseg, nnz, W, 4, first); break;
+    case 8: spmv_nnz_atomic_kernel<T, 8><<<g, threads, 0, st>>>(pos, crd, vals, x, y, nseg, nnz, W, 8, first); break;
+    case 16: spmv_nnz_atomic_kernel<T, 16><<<g, threads, 0, st>>>(pos, crd, vals, x, y, nseg, nnz, W, 16, first); break;
+    default:
+      spmv_nnz_atomic_kernel<T, 0><<<g, threads, 0, st>>>(pos, crd, vals, x, y, nseg, nnz, W, (int)TPT, first);
+  }
+  count_launch();
+  return check_cuda(cudaGetLastError(), "spmv_nnz_atomic_kernel");
+}
+
 template <typename T>
 int run_spmv(int kid, const Args& a) {
   const int32_t* pos = a.pos[0];
@@ -519,16 +539,7 @@ int run_spmv(int kid, const Args& a) {
     if (!a.ws || a.ws_bytes < need) return fail(SPX_E_WORKSPACE, "workspace %zu < %zu bytes", a.ws_bytes, need);
     int32_t* first = static_cast<int32_t*>(a.ws);
     if (int e = launch_chunk_segments(pos, M, W, nslots, first, a.stream)) return e;
-    const unsigned g = (unsigned)ncta;
-    switch (TPT) {
-      case 4: spmv_nnz_atomic_kernel<T, 4><<<g, threads, 0, a.stream>>>(pos, crd, vals, x, y, M, nnz, W, 4, first); break;
-      case 8: spmv_nnz_atomic_kernel<T, 8><<<g, threads, 0, a.stream>>>(pos, crd, vals, x, y, M, nnz, W, 8, first); break;
-      case 16: spmv_nnz_atomic_kernel<T, 16><<<g, threads, 0, a.stream>>>(pos, crd, vals, x, y, M, nnz, W, 16, first); break;
-      default:
-        spmv_nnz_atomic_kernel<T, 0><<<g, threads, 0, a.stream>>>(pos, crd, vals, x, y, M, nnz, W, (int)TPT, first);
-    }
-    count_launch();
-    return check_cuda(cudaGetLastError(), "spmv_nnz_atomic_kernel");
+    return segsum_atomic(pos, crd, vals, x, y, M, nnz, TB, W, TPT, first, a.stream);
   }
   const NnzWorkspace L = nnz_workspace(ncta, sizeof(T));
   if (!a.ws || a.ws_bytes < L.total) return fail(SPX_E_WORKSPACE, "workspace %zu < %zu bytes", a.ws_bytes, L.total);
@@ -566,6 +577,17 @@ size_t ws_spmv(int kid, const Args& a) {
   const size_t atomic_ws = (size_t)(ncta * (TB / W > 0 ? TB / W : 1) + 1) * sizeof(int32_t);
   const size_t det_ws = nnz_workspace(ncta, es).total;
   return atomic_ws > det_ws ? atomic_ws : det_ws;
+}
+
+int segsum_atomic_f32(const int32_t* pos, const int32_t* crd, const float* vals, const float* x, float* y,
+                      int64_t nseg, int64_t nnz, int64_t TB, int64_t W, int64_t TPT, const int32_t* first,
+                      cudaStream_t st) {
+  return segsum_atomic<float>(pos, crd, vals, x, y, nseg, nnz, TB, W, TPT, first, st);
+}
+int segsum_atomic_f64(const int32_t* pos, const int32_t* crd, const double* vals, const double* x, double* y,
+                      int64_t nseg, int64_t nnz, int64_t TB, int64_t W, int64_t TPT, const int32_t* first,
+                      cudaStream_t st) {
+  return segsum_atomic<double>(pos, crd, vals, x, y, nseg, nnz, TB, W, TPT, first, st);
 }
 
 int launch_spmv(int kid, const Args& a) {

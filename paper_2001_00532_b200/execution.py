@@ -298,7 +298,7 @@ class ExecStats:
         loops: dict[str, int] = {}
         guards: dict[str, int] = {}
         kid = prog.kernel_id
-        if kid in (_lib.K_SPMV_NNZ, _lib.K_SPMM_NNZ, _lib.K_SDDMM_NNZ, _lib.K_MTTKRP_NNZ):
+        if kid in (_lib.K_SPMV_NNZ, _lib.K_SPMM_NNZ, _lib.K_SDDMM_NNZ, _lib.K_MTTKRP_NNZ, _lib.K_TTV_NNZ):
             TB, W = p[0], p[1]
             blocks = _chunks(nnz, TB)
             warps = np.concatenate([_chunks(int(b), W) for b in blocks]) if len(blocks) else blocks
@@ -307,7 +307,7 @@ class ExecStats:
             loops[v["block"]] = len(blocks)
             loops[v["warp"]] = len(warps)
             guards[v["block"]] = len(blocks) * TB - nnz
-            if kid == _lib.K_SPMV_NNZ:
+            if kid in (_lib.K_SPMV_NNZ, _lib.K_TTV_NNZ):
                 T = p[2]
                 threads = np.concatenate([_chunks(int(w), T) for w in warps]) if len(warps) else warps
                 inst[v["thread"]] = threads

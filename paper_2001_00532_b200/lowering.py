@@ -479,6 +479,15 @@ def _match_spmm_like(sh: _Shape, nnz_kid: int, row_kid: int, dense_role: str, P:
 
 def _match_ttv(sh: _Shape) -> Program:
     ec = sh.ec
+    # K11 nnz-split over the leaves (the A.2 shape on fuse(i, fuse(j, k)))
+    try:
+        b, s = _nnz_split(sh, "pos[S](fuse(i,fuse(j,k)))", 3)
+        if len(sh.forest) != 4:
+            raise _NoMatch
+        kv = {"block": b["block"], "warp": b["warp"], "thread": b["thread"]}
+        return Program(sh.stmt, ec, _lib.K_TTV_NNZ, [s["TB"], s["W"], s["T"]], vars=kv)
+    except _NoMatch:
+        pass
     P = "pos[S](fuse(i,j))"
     g = sh.base_group(P)
     if g:

@@ -2,7 +2,7 @@
 path, through the public API (`corpus.build` -> `lower` -> `interpret`).
 
 1. corpus correctness: every Appendix A.1-A.11 schedule (plus the extra GPU
-   shapes K5-K10) on 30 seeded random inputs at the SPEC sizes (matrices
+   shapes K5-K11) on 30 seeded random inputs at the SPEC sizes (matrices
    40x50 density 0.1, tensors 20x25x30 density 0.05, dense operands random),
    fp64 max relative error vs the reference's `dense_eval` <= 1e-10, the
    A.1-A.11 set inside 60 s;
@@ -39,7 +39,7 @@ N = _spindle.notation
 S = _spindle.schedule
 
 APPENDIX = ["A1", "A2", "A3", "A4", "A5", "A6", "A7", "A8", "A9", "A10", "A11"]
-EXTRA = ["K5", "K6", "K7", "K9", "K10"]
+EXTRA = ["K5", "K6", "K7", "K9", "K10", "K11"]
 SEEDS = range(30)
 WIDTH = 24  # dense operand columns: not a multiple of 32, so the lane tails run
 
@@ -78,7 +78,7 @@ def _params(entry, small):
     p = {}
     if small:
         p.update(SMALL)
-        if entry.kernel == "spmv_nnz":
+        if entry.kernel in ("spmv_nnz", "ttv_nnz"):
             p.update(SMALL_SPMV_NNZ)
     if "BOUND" in entry.defaults:
         p["BOUND"] = -(-WIDTH // 32)

@@ -28,7 +28,7 @@ KIND_ENTRIES = {
     "spmv": ["A1", "A2", "A7", "A8", "A9", "SPMV0"],
     "spmm": ["A3", "A4", "A10", "A11", "K5"],
     "sddmm": ["K6", "K10"],
-    "ttv": ["K7", "TTV0"],
+    "ttv": ["K7", "K11", "TTV0"],
     "mttkrp": ["A5", "A6", "K9", "MTTKRP0"],
 }
 SPARSE = {"spmv": "A", "spmm": "A", "sddmm": "B", "ttv": "B", "mttkrp": "B"}
@@ -42,7 +42,7 @@ SMALL = {"NNZ_PER_TB": 32, "NNZ_PER_WARP": 8, "NNZ_PER_THREAD": 1, "ROWS_PER_TB"
 
 def _params(entry, case, small):
     p = dict(SMALL) if small else {}
-    if entry.name == "A2" and small:
+    if entry.name in ("A2", "K11") and small:
         p.update(NNZ_PER_TB=64, NNZ_PER_WARP=32, NNZ_PER_THREAD=1)
     if entry.name in ("A9",) and small:
         p.update(NNZ_PER_TB=128, NNZ_PER_WARP=64, NNZ_PER_THREAD=2)
@@ -88,7 +88,7 @@ def test_corpus_fp64_vs_reference_dense_eval(cuda, case, entry, small):
     # ExecStats conservation: per-instance work sums to nnz
     nnz = len(case["values"])
     for var, w in stats.instance_work.items():
-        if prog.kernel_id in (3, 4, 6, 8) or var == prog.vars.get("block"):
+        if prog.kernel_id in (3, 4, 6, 8, 11) or var == prog.vars.get("block"):
             assert int(w.sum()) == nnz, var
 
 

@@ -197,7 +197,7 @@ def main():
         elif cfg == 3:
             run_sddmm(3, M, [("K6", {"BOUND": 8}), ("K10", {})], args)
         elif cfg == 4:
-            run_csf(4, M, {"mttkrp": [("A6", {}), ("K9", {}), ("MTTKRP0", {})], "ttv": [("K7", {})]}, args)
+            run_csf(4, M, {"mttkrp": [("A6", {}), ("K9", {}), ("MTTKRP0", {})], "ttv": [("K7", {}), ("K11", {})]}, args)
         del M
         torch.cuda.empty_cache()
 
