@@ -82,6 +82,7 @@ extern "C" {
  *  8   MTTKRP nnz-split          A(i,j)=B(i,k,l)*C(k,j)*D(l,j) [0]=NNZ_PER_TB [1]=NNZ_PER_WARP [2]=WARP_SIZE [3]=bound
  *  9   MTTKRP slice-split        "                        [0]=SLICES_PER_TB [1]=WARPS_PER_TB
  *  10  SDDMM row-split           A(i,j)=B(i,j)*C(i,k)*D(j,k)  [0]=ROWS_PER_TB [1]=WARPS_PER_TB [2]=WARP_SIZE [3]=bound [7]=dense_out
+ *  11  TTV nnz-split             A(i,j)=B(i,j,k)*c(k) B:sss   [0]=NNZ_PER_TB [1]=NNZ_PER_WARP [2]=NNZ_PER_THREAD
  *
  * Operand roles: the kernels address operands by role, and slot[role] gives
  * the role's index in the Manifest tensor order (vals[]/dims[] layout):
