@@ -207,6 +207,33 @@ struct LeafRing {
 };
 
 
+// 256-bit read-only loads (LDG.E.256): a lane's 32 B run is one whole sector,
+// so a warp's request touches each sector once.  Two 16 B loads at a 32 B
+// lane stride request every sector twice (once per half), which doubles the
+// L1TEX traffic of an 8-float-per-lane row read.
+__device__ __forceinline__ void ld256_nc(const float* p, float* r) {
+  asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]), "=f"(r[7])
+               : "l"(p));
+}
+__device__ __forceinline__ void ld256_nc(const double* p, double* r) {
+  asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3]) : "l"(p));
+}
+__device__ __forceinline__ void ld256_nc_hint(const float* p, float* r, uint64_t pol) {
+  asm volatile("ld.global.nc.L2::cache_hint.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+               : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]), "=f"(r[7])
+               : "l"(p), "l"(pol));
+}
+__device__ __forceinline__ void ld256_nc_hint(const double* p, double* r, uint64_t pol) {
+  asm volatile("ld.global.nc.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+               : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3])
+               : "l"(p), "l"(pol));
+}
+
+#ifndef SPX_FRAG_LD256
+#define SPX_FRAG_LD256 1
+#endif
+
 // 16 B / 8 B vectors <-> T elements through register bit casts (no type-punned
 // stores into the per-lane arrays, which force them into local memory for fp64)
 template <typename T>
@@ -263,7 +290,10 @@ struct Frag {
     if (CONTIG) {
       const T* p = row + lane * VPL;
       constexpr int BYTES = VPL * (int)sizeof(T);
-      if constexpr (BYTES % 16 == 0) {
+      if constexpr (BYTES % 32 == 0 && SPX_FRAG_LD256) {
+#pragma unroll
+        for (int c = 0; c < BYTES / 32; ++c) ld256_nc(p + c * (32 / sizeof(T)), &v[c * (32 / sizeof(T))]);
+      } else if constexpr (BYTES % 16 == 0) {
 #pragma unroll
         for (int c = 0; c < BYTES / 16; ++c) {
           float4 q = __ldg(reinterpret_cast<const float4*>(p) + c);
@@ -292,7 +322,10 @@ struct Frag {
   // includes the lane offset), vectorised
   __device__ __forceinline__ void load_ptr(const T* __restrict__ p) {
     constexpr int BYTES = VPL * (int)sizeof(T);
-    if constexpr (BYTES % 16 == 0) {
+    if constexpr (BYTES % 32 == 0 && SPX_FRAG_LD256) {
+#pragma unroll
+      for (int c = 0; c < BYTES / 32; ++c) ld256_nc(p + c * (32 / sizeof(T)), &v[c * (32 / sizeof(T))]);
+    } else if constexpr (BYTES % 16 == 0) {
 #pragma unroll
       for (int c = 0; c < BYTES / 16; ++c) {
         float4 q = __ldg(reinterpret_cast<const float4*>(p) + c);
@@ -313,7 +346,10 @@ struct Frag {
   // load_ptr with an L2 eviction-priority policy on the 16 B vector path
   __device__ __forceinline__ void load_ptr_hint(const T* __restrict__ p, uint64_t pol) {
     constexpr int BYTES = VPL * (int)sizeof(T);
-    if constexpr (BYTES % 16 == 0) {
+    if constexpr (BYTES % 32 == 0 && SPX_FRAG_LD256) {
+#pragma unroll
+      for (int c = 0; c < BYTES / 32; ++c) ld256_nc_hint(p + c * (32 / sizeof(T)), &v[c * (32 / sizeof(T))], pol);
+    } else if constexpr (BYTES % 16 == 0) {
 #pragma unroll
       for (int c = 0; c < BYTES / 16; ++c) {
         float4 q = ld_f4_hint(reinterpret_cast<const float4*>(p) + c, pol);
@@ -327,7 +363,11 @@ struct Frag {
   // gather with an L2 eviction-priority policy (16 B vector path)
   __device__ __forceinline__ void load_hint(const T* __restrict__ row, int lane, int ncols, uint64_t pol) {
     constexpr int BYTES = VPL * (int)sizeof(T);
-    if constexpr (CONTIG && BYTES % 16 == 0) {
+    if constexpr (CONTIG && BYTES % 32 == 0 && SPX_FRAG_LD256) {
+      const T* p = row + lane * VPL;
+#pragma unroll
+      for (int c = 0; c < BYTES / 32; ++c) ld256_nc_hint(p + c * (32 / sizeof(T)), &v[c * (32 / sizeof(T))], pol);
+    } else if constexpr (CONTIG && BYTES % 16 == 0) {
       const T* p = row + lane * VPL;
 #pragma unroll
       for (int c = 0; c < BYTES / 16; ++c) {
