@@ -755,8 +755,8 @@ int run_ttv_nnz(const Args& a) {
   const T* vals = static_cast<const T*>(a.vals[0]);
   const T* cv = static_cast<const T*>(a.vals[1]);
   int e;
-  if constexpr (sizeof(T) == 4) e = segsum_atomic_f32(c.pos2, c.crd2, vals, cv, fsum, c.F, c.nnz, TB, W, TPT, first, a.stream);
-  else e = segsum_atomic_f64(c.pos2, c.crd2, vals, cv, fsum, c.F, c.nnz, TB, W, TPT, first, a.stream);
+  if constexpr (sizeof(T) == 4) e = segsum_atomic_f32(c.pos2, c.crd2, vals, cv, fsum, c.F, c.nnz, TB, W, TPT, first, a.stream, a.dims[0][2]);
+  else e = segsum_atomic_f64(c.pos2, c.crd2, vals, cv, fsum, c.F, c.nnz, TB, W, TPT, first, a.stream, a.dims[0][2]);
   if (e) return e;
   ttv_scatter_kernel<T><<<(unsigned)ceil_div(c.F, 256), 256, 0, a.stream>>>(c.crd0, c.pos1, c.crd1, fsum, A, c.S,
                                                                           c.F, J);

@@ -69,10 +69,10 @@ inline NnzWorkspace nnz_workspace(int64_t ncta, size_t es, int64_t vals_per_cta 
 // the Atomics nnz-split segment sum of spx_spmv.cu (y zeroed by the caller)
 int segsum_atomic_f32(const int32_t* pos, const int32_t* crd, const float* vals, const float* x, float* y,
                       int64_t nseg, int64_t nnz, int64_t TB, int64_t W, int64_t TPT, const int32_t* first,
-                      cudaStream_t st);
+                      cudaStream_t st, int64_t xlen);
 int segsum_atomic_f64(const int32_t* pos, const int32_t* crd, const double* vals, const double* x, double* y,
                       int64_t nseg, int64_t nnz, int64_t TB, int64_t W, int64_t TPT, const int32_t* first,
-                      cudaStream_t st);
+                      cudaStream_t st, int64_t xlen);
 int launch_chunk_segments(const int32_t* pos, int64_t nseg, int64_t chunk, int64_t nchunks, int32_t* first,
                           cudaStream_t stream);
 

@@ -355,12 +355,24 @@ constexpr int kWarpPos = 320;  // pos entries staged per warp
 #ifndef SPX_SPMV_MINB
 #define SPX_SPMV_MINB 2
 #endif
-template <typename T, int TPT>
+// XS: x is short enough to sit in shared memory (the TTV vector c): it is
+// staged once per CTA and the per-position gathers become shared-memory
+// reads -- random 4/8 B gathers through L1 cost one L1TEX wavefront each,
+// even when they hit.
+template <typename T, int TPT, bool XS = false>
 __global__ void __launch_bounds__(kMaxThreads, SPX_SPMV_MINB) spmv_nnz_atomic_kernel(
     const int32_t* __restrict__ pos, const int32_t* __restrict__ crd, const T* __restrict__ vals,
     const T* __restrict__ x, T* __restrict__ y, int64_t M, int64_t nnz, int64_t W, int tpt_rt,
-    const int32_t* __restrict__ first) {
+    const int32_t* __restrict__ first, int64_t xlen = 0) {
   __shared__ int32_t s_pos_all[kMaxWarps][kWarpPos];
+  extern __shared__ __align__(16) unsigned char smem_x[];
+  const T* __restrict__ xr = x;
+  if constexpr (XS) {
+    T* sx = reinterpret_cast<T*>(smem_x);
+    for (int64_t i = threadIdx.x; i < xlen; i += blockDim.x) sx[i] = __ldg(x + i);
+    __syncthreads();
+    xr = sx;
+  }
   const int tpt = TPT > 0 ? TPT : tpt_rt;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int32_t* s_pos = s_pos_all[warp];
@@ -378,7 +390,7 @@ __global__ void __launch_bounds__(kMaxThreads, SPX_SPMV_MINB) spmv_nnz_atomic_ke
   if constexpr (TPT > 0) {
     load_thread_chunk<T, TPT>(crd, vals, a, n, cc, vv);
 #pragma unroll
-    for (int k = 0; k < TPT; ++k) xv[k] = __ldg(x + cc[k]);  // cc = 0 past n: harmless
+    for (int k = 0; k < TPT; ++k) xv[k] = XS ? xr[cc[k]] : __ldg(x + cc[k]);  // cc = 0 past n: harmless
   }
   const int rlo = __ldg(first + q), rhi = __ldg(first + q + 1);
   const int nstage = rhi - rlo + 2;  // pos[rlo .. rhi+1]
@@ -431,7 +443,8 @@ __global__ void __launch_bounds__(kMaxThreads, SPX_SPMV_MINB) spmv_nnz_atomic_ke
       }
     } else {
       for (int p = a; p < e; ++p) {
-        const T prod = __ldcs(vals + p) * __ldg(x + __ldcs(crd + p));
+        const int cp = __ldcs(crd + p);
+        const T prod = __ldcs(vals + p) * (XS ? xr[cp] : __ldg(x + cp));
         while (p >= rend) {
           close_row();
           acc = T(0);
@@ -482,9 +495,18 @@ __global__ void spmv_fixup_kernel(const int32_t* __restrict__ carry_row, const T
 // (rows) and the nnz-split TTV (fibers of a CSF tensor) share it.
 template <typename T>
 int segsum_atomic(const int32_t* pos, const int32_t* crd, const T* vals, const T* x, T* y, int64_t nseg,
-                  int64_t nnz, int64_t TB, int64_t W, int64_t TPT, const int32_t* first, cudaStream_t st) {
+                  int64_t nnz, int64_t TB, int64_t W, int64_t TPT, const int32_t* first, cudaStream_t st,
+                  int64_t xlen = 0) {
   const int threads = (int)(TB / TPT);
   const unsigned g = (unsigned)(nnz == 0 ? 1 : ceil_div(nnz, TB));
+  // x in shared memory when it is short (<= 16 KB) and no larger than the
+  // (crd, vals) bytes a CTA streams (every CTA stages all of x)
+  const size_t xbytes = (size_t)xlen * sizeof(T);
+  if (TPT == 8 && xlen > 0 && xbytes <= 16384 && (size_t)TB * (4 + sizeof(T)) >= xbytes) {
+    spmv_nnz_atomic_kernel<T, 8, true><<<g, threads, xbytes, st>>>(pos, crd, vals, x, y, nseg, nnz, W, 8, first, xlen);
+    count_launch();
+    return check_cuda(cudaGetLastError(), "spmv_nnz_atomic_kernel");
+  }
   switch (TPT) {
     case 4: spmv_nnz_atomic_kernel<T, 4><<<g, threads, 0, st>>>(pos, crd, vals, x, y, nseg, nnz, W, 4, first); break;
     case 8: spmv_nnz_atomic_kernel<T, 8><<<g, threads, 0, st>>>(pos, crd, vals, x, y, nseg, nnz, W, 8, first); break;
@@ -539,7 +561,7 @@ int run_spmv(int kid, const Args& a) {
     if (!a.ws || a.ws_bytes < need) return fail(SPX_E_WORKSPACE, "workspace %zu < %zu bytes", a.ws_bytes, need);
     int32_t* first = static_cast<int32_t*>(a.ws);
     if (int e = launch_chunk_segments(pos, M, W, nslots, first, a.stream)) return e;
-    return segsum_atomic(pos, crd, vals, x, y, M, nnz, TB, W, TPT, first, a.stream);
+    return segsum_atomic(pos, crd, vals, x, y, M, nnz, TB, W, TPT, first, a.stream, a.dims[1][0]);
   }
   const NnzWorkspace L = nnz_workspace(ncta, sizeof(T));
   if (!a.ws || a.ws_bytes < L.total) return fail(SPX_E_WORKSPACE, "workspace %zu < %zu bytes", a.ws_bytes, L.total);
@@ -581,13 +603,13 @@ size_t ws_spmv(int kid, const Args& a) {
 
 int segsum_atomic_f32(const int32_t* pos, const int32_t* crd, const float* vals, const float* x, float* y,
                       int64_t nseg, int64_t nnz, int64_t TB, int64_t W, int64_t TPT, const int32_t* first,
-                      cudaStream_t st) {
-  return segsum_atomic<float>(pos, crd, vals, x, y, nseg, nnz, TB, W, TPT, first, st);
+                      cudaStream_t st, int64_t xlen) {
+  return segsum_atomic<float>(pos, crd, vals, x, y, nseg, nnz, TB, W, TPT, first, st, xlen);
 }
 int segsum_atomic_f64(const int32_t* pos, const int32_t* crd, const double* vals, const double* x, double* y,
                       int64_t nseg, int64_t nnz, int64_t TB, int64_t W, int64_t TPT, const int32_t* first,
-                      cudaStream_t st) {
-  return segsum_atomic<double>(pos, crd, vals, x, y, nseg, nnz, TB, W, TPT, first, st);
+                      cudaStream_t st, int64_t xlen) {
+  return segsum_atomic<double>(pos, crd, vals, x, y, nseg, nnz, TB, W, TPT, first, st, xlen);
 }
 
 int launch_spmv(int kid, const Args& a) {
