@@ -95,7 +95,8 @@ def baseline_table(s: str) -> str:
             (2, "spmm_nnz", "**SpMM nnz-split (A.4)**"), (2, "spmm_row", "SpMM warp-per-row (K5)"),
             (3, "sddmm_nnz", "SDDMM nnz-split (K6)"), (3, "sddmm_row", "SDDMM row-split (K10)"),
             (4, "mttkrp_nnz", "MTTKRP nnz-split (A.6)"), (4, "mttkrp_slice", "MTTKRP slice-split (A.5/K9)"),
-            (4, "ttv_fiber", "TTV fiber-split (K7)"), (5, "spmv_nnz", "SpMV nnz-split (A.2/A.9)"),
+            (4, "ttv_fiber", "TTV fiber-split (K7)"), (4, "ttv_nnz", "TTV nnz-split (K11)"),
+            (5, "spmv_nnz", "SpMV nnz-split (A.2/A.9)"),
             (5, "spmv_warp", "SpMV warp-per-row (A.8)"), (5, "spmv_row", "SpMV thread-per-row (A.7)")]
     b = json.load(open(PROF / "r01_bench.json"))
     cpu = b["cpu_baseline"]
