@@ -23,6 +23,9 @@
 #ifndef SPX_SDDMM_ROW_UR
 #define SPX_SDDMM_ROW_UR 4   // cfg3 K10: 7.8 ms (2 rows, 2 CTAs/SM) -> 5.7 ms
 #endif
+#ifndef SPX_SDDMM_UN
+#define SPX_SDDMM_UN 2  // D rows (1 KB) in flight per warp; 4 spills at 64 registers (cfg3 1.68 vs 1.57 ms)
+#endif
 #ifndef SPX_SDDMM_MINB
 #define SPX_SDDMM_MINB 2
 #endif
@@ -243,7 +246,7 @@ int run_sddmm(int kid, const Args& a) {
       return fail(SPX_E_WORKSPACE, "workspace %zu < %zu bytes", a.ws_bytes, (size_t)(nchunks + 1) * 4);
     int32_t* first = static_cast<int32_t*>(a.ws);
     if (int e = launch_chunk_segments(pos, M, W, nchunks, first, a.stream)) return e;
-    constexpr int UN = VPL * (int)sizeof(T) >= 32 ? 2 : 4;  // D rows in flight per warp
+    constexpr int UN = VPL * (int)sizeof(T) >= 32 ? SPX_SDDMM_UN : 4;  // D rows in flight per warp
     sddmm_nnz_kernel<T, VPL, CONTIG, UN><<<(unsigned)ncta, (unsigned)(wpc * 32), wpc * LeafRing<T, 4>::kBytes,
                                            a.stream>>>(pos, crd, vals, Cm, Dm, out, M, N, K, nnz, W, (int)wpc,
                                                        dense, first);
