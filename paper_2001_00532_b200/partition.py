@@ -114,13 +114,28 @@ def _csf_sub(pos: dict, crd: dict, vals: np.ndarray, p0: int, p1: int) -> CsfSha
                     {0: crd[0][s0:s1 + 1], 1: crd[1][f0:f1 + 1], 2: crd[2][p0:p1]}, vals[p0:p1], p0, p1)
 
 
-def csf_shards(pos: dict, crd: dict, vals: np.ndarray, ndev: int, exact: bool = False) -> list[CsfShard]:
+def csf_shards(pos: dict, crd: dict, vals: np.ndarray, ndev: int, exact: bool = False,
+               fiber_weight: float = 0.0) -> list[CsfShard]:
+    """Slice shards by the `divide` rule on the leaves (or leaf-exact shards).
+    `fiber_weight` > 0 balances leaves + fiber_weight * fibers instead: the
+    nnz-split MTTKRP pays a fixed cost per fiber end, so slices of short
+    fibers cost more per leaf (the same rule on that cost, snapped to slices)."""
     nnz = len(vals)
     if exact:
         chunk = -(-nnz // ndev) if nnz else 0
         return [_csf_sub(pos, crd, vals, min(g * chunk, nnz), min((g + 1) * chunk, nnz)) for g in range(ndev)]
     seg_start = pos[2][pos[1][:-1].astype(np.int64)]
-    R = partition(seg_start, nnz, ndev)
+    if fiber_weight > 0:
+        fib_start = pos[1][:-1].astype(np.int64)
+        cost = seg_start.astype(np.float64) + fiber_weight * fib_start
+        total = nnz + fiber_weight * (len(pos[2]) - 1)
+        chunk = total / ndev
+        R = np.empty(ndev + 1, dtype=np.int64)
+        R[0], R[ndev] = 0, len(seg_start)
+        for g in range(1, ndev):
+            R[g] = int(np.searchsorted(cost, min(g * chunk, total), side="left"))
+    else:
+        R = partition(seg_start, nnz, ndev)
     pos2 = pos[2].astype(np.int64)
     pos1 = pos[1].astype(np.int64)
     out = []

@@ -116,8 +116,8 @@ def test_csr_shards_cover_matrix():
     assert max(s.nnz for s in shards) <= chunk + lens.max()
 
 
-@pytest.mark.parametrize("exact", [False, True])
-def test_csf_shards_preserve_mttkrp(exact):
+@pytest.mark.parametrize("exact,weight", [(False, 0.0), (True, 0.0), (False, 25.0)])
+def test_csf_shards_preserve_mttkrp(exact, weight):
     from paper_2001_00532_b200 import synth
 
     T = synth.bitskew_csf(5, 3000, seed=11, cache=False)
@@ -125,7 +125,7 @@ def test_csf_shards_preserve_mttkrp(exact):
     C = rng.random((32, 8))
     D = rng.random((32, 8))
     full = O.mttkrp(T.dims, T.pos, T.crd, T.vals, C, D)
-    parts = csf_shards(T.pos, T.crd, T.vals, 3, exact=exact)
+    parts = csf_shards(T.pos, T.crd, T.vals, 3, exact=exact, fiber_weight=weight)
     assert sum(p.nnz for p in parts) == T.nnz
     acc = np.zeros_like(full)
     for p in parts:
@@ -137,3 +137,17 @@ def test_comm_available_is_safe_without_a_gpu():
     from paper_2001_00532_b200 import _lib
 
     assert _lib.load().spx_comm_available() in (0, 1)
+
+
+def test_csf_fiber_weight_moves_cuts_toward_short_fibers():
+    from paper_2001_00532_b200 import synth
+
+    T = synth.bitskew_csf(8, 40_000, seed=3, cache=False)
+    plain = csf_shards(T.pos, T.crd, T.vals, 4)
+    weighted = csf_shards(T.pos, T.crd, T.vals, 4, fiber_weight=25.0)
+    fibers = lambda p: len(p.pos[2]) - 1  # noqa: E731
+    cost = lambda p: p.nnz + 25.0 * fibers(p)  # noqa: E731
+    # the weighted cut balances leaves + 25 * fibers at least as well as the plain one
+    spread = lambda parts: max(map(cost, parts)) / (sum(map(cost, parts)) / len(parts))  # noqa: E731
+    assert spread(weighted) <= spread(plain) + 1e-9
+    assert sum(p.nnz for p in weighted) == T.nnz

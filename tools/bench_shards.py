@@ -54,6 +54,7 @@ def main():
     ap.add_argument("--cfg", default="2,5,4")
     ap.add_argument("--reps", type=int, default=9)
     ap.add_argument("--exact", action="store_true", help="leaf-exact CSF shards (MTTKRP partials all-reduced)")
+    ap.add_argument("--fiber-weight", type=float, default=0.0, help="balance leaves + w * fibers across CSF shards")
     args = ap.parse_args()
     dev = torch.device("cuda")
     for cfg in (int(c) for c in args.cfg.split(",")):
@@ -82,7 +83,7 @@ def main():
             flops = 2.0 * M.nnz
             name = "SpMV A.2"
         else:
-            name = "MTTKRP A.6" + (" (leaf-exact shards)" if args.exact else "")
+            name = "MTTKRP A.6" + (" (leaf-exact shards)" if args.exact else "") + (f" (fiber weight {args.fiber_weight:g})" if args.fiber_weight else "")
             C = DeviceTensor.dense(synth.dense((2048, 32), seed=401, dtype=np.float32), device=dev)
             D = DeviceTensor.dense(synth.dense((2048, 32), seed=402, dtype=np.float32), device=dev)
             prog = lower(corpus.build("A6"))
@@ -91,7 +92,7 @@ def main():
             res = {}
             for G in (1, 2, 4, 8):
                 ts = []
-                for sh in csf_shards(M.pos, M.crd, M.vals, G, exact=args.exact):
+                for sh in csf_shards(M.pos, M.crd, M.vals, G, exact=args.exact, fiber_weight=args.fiber_weight):
                     Bd = DeviceTensor.from_arrays(M.dims, "sss", sh.pos, sh.crd, sh.vals.astype(np.float32),
                                                   device=dev, dtype="f32")
                     o = torch.empty(2048 * 32, dtype=torch.float32, device=dev)

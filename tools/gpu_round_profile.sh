@@ -9,4 +9,5 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:spmm
 timeout 1200 python tools/bench_configs.py > gpurun_out/rp_configs.jsonl 2> gpurun_out/rp_configs.err
 timeout 600 python tools/bench_loadbal.py > gpurun_out/rp_loadbal.jsonl 2> gpurun_out/rp_loadbal.err
 timeout 900 python tools/bench_shards.py > gpurun_out/rp_shards.jsonl 2> gpurun_out/rp_shards.err
+timeout 600 python tools/bench_shards.py --cfg 4 --fiber-weight 25 > gpurun_out/rp_shards_weighted.jsonl 2>> gpurun_out/rp_shards.err
 cat gpurun_out/rp_pytest.txt gpurun_out/rp_smoke.txt gpurun_out/rp_bench.json

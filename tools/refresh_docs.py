@@ -21,7 +21,8 @@ PROF = ROOT / "profiles"
 def copy_profiles():
     pairs = {"rp_configs.jsonl": "r01_configs.jsonl", "rp_bench.json": "r01_bench.json",
              "rp_launches.csv": "r01_launches.csv", "rp_loadbal.jsonl": "r01_loadbal.jsonl",
-             "rp_shards.jsonl": "r01_shard_scaling.jsonl", "rp_pack.jsonl": "r01_pack.jsonl"}
+             "rp_shards.jsonl": "r01_shard_scaling.jsonl", "rp_pack.jsonl": "r01_pack.jsonl",
+             "rp_shards_weighted.jsonl": "r01_shard_scaling_weighted.jsonl"}
     for src, dst in pairs.items():
         if (OUT / src).exists() and (OUT / src).stat().st_size:
             shutil.copy(OUT / src, PROF / dst)
