@@ -262,7 +262,7 @@ def main():
     sampler = ClockSampler(local)
     sampler.start()
     # keep the GPU busy ~1 s so the clock sampler sees the loaded state
-    t_end = time.perf_counter() + (0.0 if args.profile else 1.0)
+    t_end = time.perf_counter() + (0.0 if args.profile else float(os.environ.get("SPX_BENCH_PRELOAD_S", "1.0")))
     while time.perf_counter() < t_end:
         for _ in range(20):
             ex.launch()
