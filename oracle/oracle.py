@@ -20,6 +20,7 @@ from __future__ import annotations
 import ctypes
 import os
 import subprocess
+import tempfile
 from pathlib import Path
 
 import numpy as np
@@ -40,13 +41,43 @@ def build(force: bool = False) -> Path:
 
 
 _lib = None
+_native = None
 
 
-def lib():
+def build_native() -> Path:
+    """The timing build: gcc -O3 -march=native -fopenmp,
+    compiled on the host that runs it (the GPU box's CPU, not this
+    container's) into a fresh temporary directory."""
+    out = Path(tempfile.mkdtemp(prefix="spx_oracle_")) / "liboracle_native.so"
+    subprocess.run(["gcc", "-O3", "-march=native", "-fopenmp", "-fPIC", "-shared", "-o", str(out), str(SRC)],
+                   check=True)
+    return out
+
+
+def use_native() -> str:
+    """Switch this process to the -march=native build for timing.  Call
+    before the first oracle call: OpenMP reads OMP_PROC_BIND / OMP_PLACES /
+    OMP_NUM_THREADS when libgomp initialises (set here unless the caller
+    already did).  Returns a description of the build."""
+    global _lib, _native
+    os.environ.setdefault("OMP_PROC_BIND", "close")
+    os.environ.setdefault("OMP_PLACES", "cores")
+    os.environ.setdefault("OMP_NUM_THREADS", str(len(os.sched_getaffinity(0))))
+    if _native is None:
+        _native = build_native()
+    _lib = None
+    lib(_native)
+    return (f"gcc -O3 -march=native -fopenmp, OMP_PROC_BIND={os.environ['OMP_PROC_BIND']} "
+            f"OMP_PLACES={os.environ['OMP_PLACES']} OMP_NUM_THREADS={os.environ['OMP_NUM_THREADS']}")
+
+
+def lib(path: Path | None = None):
     global _lib
     if _lib is None:
-        build()
-        L = ctypes.CDLL(str(LIB))
+        if path is None:
+            build()
+            path = LIB
+        L = ctypes.CDLL(str(path))
         vp, i64 = ctypes.c_void_p, ctypes.c_int64
         L.orc_threads.restype = ctypes.c_int
         L.orc_search_segment.argtypes = [vp, i64, i64, i64]

@@ -64,6 +64,13 @@ __device__ __forceinline__ float4 ld_f4_hint(const void* p, uint64_t pol) {
       : "l"(p), "l"(pol));
   return r;
 }
+__device__ __forceinline__ int4 ld_i4_hint(const void* p, uint64_t pol) {
+  int4 r;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+      : "l"(p), "l"(pol));
+  return r;
+}
 __device__ __forceinline__ void st_f4_hint(void* p, float4 v, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
                "f"(v.w), "l"(pol)

@@ -716,6 +716,203 @@ __global__ void ttv_scatter_kernel(const int32_t* __restrict__ crd0, const int32
   A[(int64_t)__ldg(crd0 + lo) * J + __ldg(crd1 + f)] = fsum[f];
 }
 
+
+// ---------------------------------------------------------------------------
+// K11 TTV nnz-split, streaming form.  The leaf level is a CSR whose rows are
+// the fibers (pos2 the row pointer); A(i,j) = sum_k B(i,j,k) c(k) is a
+// segmented sum over the leaf stream, and the stream is the only HBM-sized
+// traffic (8 B per fp32 leaf: crd2 + vals), so the kernel is built to keep
+// that stream moving:
+//  * the schedule's block (NNZ_PER_TB leaves) is a tile; a persistent CTA
+//    takes a contiguous run of tiles, so the fiber open at the next tile's
+//    first leaf (and its slice) falls out of the current tile's setup -- no
+//    search per tile, no chunk table, no extra launch;
+//  * a thread (NNZ_PER_THREAD = LPT leaves) loads its coordinates and values
+//    with 16 B vector loads before the tile setup runs (the loads are in
+//    flight meanwhile), c is staged in shared memory;
+//  * tile setup: the fibers starting inside the tile (pos2 in (p0, p1)),
+//    compacted to the non-empty ones, with their output offsets
+//    crd0[slice]*J + crd1[f] (slice tracked from the previous one: "step:
+//    while-advance over pos boundaries"), go to shared memory;
+//  * a thread folds its leaves fiber by fiber (Track recovery: the next
+//    fiber start is compared against the position), stores fibers that
+//    start and end inside it, and a segmented warp scan joins the partials
+//    that cross lanes; fibers crossing a warp boundary are completed with
+//    one red.add per warp end (the schedule's Atomics strategy on the
+//    thread loop; A is zeroed first).
+// ---------------------------------------------------------------------------
+template <typename T, int LPT, typename OffT>
+__global__ void __launch_bounds__(512) ttv_stream_kernel(
+    const int32_t* __restrict__ crd0, const int32_t* __restrict__ pos1, const int32_t* __restrict__ crd1,
+    const int32_t* __restrict__ pos2, const int32_t* __restrict__ crd2, const T* __restrict__ vals,
+    const T* __restrict__ c, T* __restrict__ A, int S, int F, int nnz, int64_t J, int K, int TB, int ntiles,
+    int csmem) {
+  static_assert(LPT % 4 == 0 && LPT <= 16, "whole 16 B coordinate vectors per thread");
+  constexpr int VCH = LPT * (int)sizeof(T) / 16;  // 16 B value vectors per thread
+  constexpr int VPC = 16 / (int)sizeof(T);
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x;
+  // layout: starts[TB] | offs[TB] | c[K] (when staged)
+  int* starts = reinterpret_cast<int*>(sm);
+  OffT* offs = reinterpret_cast<OffT*>(sm + (size_t)TB * 4);
+  T* sc = reinterpret_cast<T*>(sm + (size_t)TB * 4 + (size_t)TB * sizeof(OffT));
+  __shared__ int s_warp_cnt[kMaxWarps + 1];
+  __shared__ int s_nf, s_fnext, s_snext;
+  __shared__ OffT s_off_in;
+  if (csmem) {
+    for (int k = tid; k < K; k += nthr) sc[k] = __ldg(c + k);
+  }
+  // this CTA's contiguous tile range
+  const int t_begin = (int)(((int64_t)ntiles * blockIdx.x) / gridDim.x);
+  const int t_end = (int)(((int64_t)ntiles * (blockIdx.x + 1)) / gridDim.x);
+  if (t_begin >= t_end) return;
+  // fiber and slice open at the first tile's first leaf (SearchSegment, ir.py:178-190)
+  if (warp == 0) {
+    const int f = (int)warp_search_segment(pos2, 0, F, (int64_t)t_begin * TB, lane);
+    const int s = (int)warp_search_segment(pos1, 0, S, f, lane);
+    if (lane == 0) {
+      s_fnext = f;
+      s_snext = s;
+    }
+  }
+  __syncthreads();
+  const uint64_t pol = l2_evict_first();
+  for (int t = t_begin; t < t_end; ++t) {
+    const int p0 = t * TB;
+    const int p1 = min(p0 + TB, nnz);
+    const int f_lo = s_fnext, s_lo = s_snext;
+    // -- the thread's leaves: issue the loads first ------------------------
+    const int q0 = p0 + tid * LPT;
+    int kk[LPT];
+    T v[LPT];
+    if (q0 + LPT <= p1) {
+#pragma unroll
+      for (int h = 0; h < LPT / 4; ++h) {
+        const int4 k4 = ld_i4_hint(crd2 + q0 + 4 * h, pol);
+        kk[4 * h] = k4.x;
+        kk[4 * h + 1] = k4.y;
+        kk[4 * h + 2] = k4.z;
+        kk[4 * h + 3] = k4.w;
+      }
+#pragma unroll
+      for (int h = 0; h < VCH; ++h) unpack16<T>(v + h * VPC, ld_f4_hint(vals + q0 + h * VPC, pol));
+    } else {
+#pragma unroll
+      for (int j = 0; j < LPT; ++j) {
+        const bool in = q0 + j < p1;
+        kk[j] = in ? __ldg(crd2 + q0 + j) : 0;
+        v[j] = in ? __ldg(vals + q0 + j) : T(0);
+      }
+    }
+    // -- tile setup: non-empty fibers starting in (p0, p1), compacted --------
+    if (tid == 0) {
+      s_nf = 0;
+      s_off_in = (OffT)__ldg(crd0 + s_lo) * (OffT)J + (OffT)__ldg(crd1 + f_lo);
+    }
+    __syncthreads();
+    int sl = s_lo;  // slice of this thread's candidate fiber (monotone over batches)
+    for (int base = f_lo + 1;; base += nthr) {
+      const int f = base + tid;
+      const int q = f < F ? __ldg(pos2 + f) : INT_MAX;
+      const int qn = f < F ? __ldg(pos2 + f + 1) : INT_MAX;
+      const bool le = q <= p1;  // starts at or before the next tile's first leaf
+      const bool take = q < p1 && qn > q;  // a non-empty fiber starting in the tile
+      int s = sl;
+      if (le && f < F) {
+        // slice of fiber f: the largest s with pos1[s] <= f, from the last one
+        if (__ldg(pos1 + s + 1) <= f) s = (int)search_segment(pos1, s + 1, S, f);
+      }
+      const unsigned bal = __ballot_sync(kFull, take);
+      if (lane == 0) s_warp_cnt[warp] = __popc(bal);
+      const int nle = __syncthreads_count(le);
+      if (tid == 0) {
+        int acc = s_nf;
+        for (int w = 0; w < (nthr >> 5); ++w) {
+          const int x = s_warp_cnt[w];
+          s_warp_cnt[w] = acc;
+          acc += x;
+        }
+        s_warp_cnt[kMaxWarps] = acc;
+      }
+      __syncthreads();
+      if (take) {
+        const int r = s_warp_cnt[warp] + __popc(bal & ((1u << lane) - 1u));
+        starts[r] = q;
+        offs[r] = (OffT)__ldg(crd0 + s) * (OffT)J + (OffT)__ldg(crd1 + f);
+      }
+      if (le && (tid == nle - 1) && f < F) {  // the last fiber starting <= p1: open at the next tile
+        s_fnext = f;
+        s_snext = s;
+      }
+      __syncthreads();
+      if (tid == 0) s_nf = s_warp_cnt[kMaxWarps];
+      if (nle < nthr) break;
+      sl = s;  // every candidate was <= p1: the next batch continues from here
+    }
+    __syncthreads();
+    const int nf = s_nf;
+    const OffT off_in = s_off_in;
+    // -- fold ----------------------------------------------------------------
+    // r = the fiber (rank in starts[], -1 = the tile's incoming fiber) open
+    // just before my first leaf
+    // (strictly before q0: a fiber starting at q0 is a start at my j = 0)
+    int lo = 0, hi = nf;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (starts[mid] < q0) lo = mid + 1;
+      else hi = mid;
+    }
+    int r = lo - 1;
+    const int r_first = r;
+    int next = r + 1 < nf ? starts[r + 1] : INT_MAX;
+    T acc = T(0), lead = T(0);
+    bool seen = false, lead_empty = false;
+#pragma unroll
+    for (int j = 0; j < LPT; ++j) {
+      const T x = v[j] * (csmem ? sc[kk[j]] : __ldg(c + kk[j]));
+      if (q0 + j == next) {  // a fiber starts here (Track: advance to it)
+        if (!seen) {
+          lead = acc;
+          lead_empty = j == 0;
+          seen = true;
+        } else {
+          A[offs[r]] = acc;  // started and ended inside this thread
+        }
+        ++r;
+        next = r + 1 < nf ? starts[r + 1] : INT_MAX;
+        acc = T(0);
+      }
+      acc += x;
+    }
+    // -- warp: join the partials that cross lanes ----------------------------
+    // value leaving each lane: its open segment; a lane that saw a start
+    // begins a new scan segment
+    T sv = seen ? acc : lead + acc;
+    if (!seen) lead = acc;
+    const unsigned heads = __ballot_sync(kFull, seen);
+    const int seg = 31 - __clz((heads | 1u) & (0xffffffffu >> (31 - lane)));
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const T y = __shfl_up_sync(kFull, sv, o);
+      if (lane - o >= seg && lane >= o) sv += y;
+    }
+    T in = __shfl_up_sync(kFull, sv, 1);  // open partial arriving at my first leaf
+    if (lane == 0) in = T(0);
+    if (seen) {
+      // my first start closes fiber r_first (it holds in + lead in this warp)
+      const bool started_here = (heads & ((1u << lane) - 1u)) != 0u;
+      const OffT o = r_first >= 0 ? offs[r_first] : off_in;
+      if (started_here) A[o] = in + lead;
+      else if (!(lane == 0 && lead_empty)) atomicAdd(A + o, in + lead);
+    }
+    if (lane == 31) {  // the fiber open at the warp's end continues past it
+      const OffT o = r >= 0 ? offs[r] : off_in;
+      atomicAdd(A + o, sv);
+    }
+    __syncthreads();  // starts/offs are rewritten by the next tile
+  }
+}
+
 struct TtvNnzLayout {
   size_t fsum, first, total;
   int64_t nslots;
@@ -733,6 +930,46 @@ TtvNnzLayout ttv_nnz_layout(const Args& a) {
   return L;
 }
 
+
+template <typename T, int LPT, typename OffT>
+int launch_ttv_stream(const Args& a, const Csf& c, int64_t TB) {
+  const int64_t J = a.dims[0][1], K = a.dims[0][2];
+  const int threads = (int)(TB / LPT);
+  const int csmem = (size_t)K * sizeof(T) <= 16384 ? 1 : 0;
+  const size_t smem = (size_t)TB * (4 + sizeof(OffT)) + (csmem ? (size_t)K * sizeof(T) : 0);
+  auto kern = ttv_stream_kernel<T, LPT, OffT>;
+  static thread_local size_t attr_set = 0;
+  if (smem > 48 * 1024 && smem > attr_set) {
+    if (int e = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                           "smem attribute"))
+      return e;
+    attr_set = smem;
+  }
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+  if (per_sm < 1) per_sm = 1;
+  const int64_t ntiles = ceil_div(c.nnz, TB);
+  const int64_t grid = min((int64_t)num_sms() * per_sm, ntiles);
+  kern<<<(unsigned)grid, (unsigned)threads, smem, a.stream>>>(
+      c.crd0, c.pos1, c.crd1, c.pos2, c.crd2, static_cast<const T*>(a.vals[0]), static_cast<const T*>(a.vals[1]),
+      static_cast<T*>(a.out), (int)c.S, (int)c.F, (int)c.nnz, J, (int)K, (int)TB, (int)ntiles, csmem);
+  count_launch();
+  return check_cuda(cudaGetLastError(), "ttv_stream_kernel");
+}
+
+template <typename T>
+int run_ttv_stream(const Args& a, const Csf& c, int64_t TB, int TPT) {
+  const bool off32 = a.dims[0][0] * a.dims[0][1] < (int64_t)INT32_MAX;
+  switch (TPT * 2 + (off32 ? 1 : 0)) {
+    case 9: return launch_ttv_stream<T, 4, int32_t>(a, c, TB);
+    case 8: return launch_ttv_stream<T, 4, int64_t>(a, c, TB);
+    case 17: return launch_ttv_stream<T, 8, int32_t>(a, c, TB);
+    case 16: return launch_ttv_stream<T, 8, int64_t>(a, c, TB);
+    case 33: return launch_ttv_stream<T, 16, int32_t>(a, c, TB);
+    default: return launch_ttv_stream<T, 16, int64_t>(a, c, TB);
+  }
+}
+
 template <typename T>
 int run_ttv_nnz(const Args& a) {
   const Csf c = csf_of(a);
@@ -746,6 +983,7 @@ int run_ttv_nnz(const Args& a) {
                 "TTV nnz-split needs NNZ_PER_WARP == 32*NNZ_PER_THREAD and NNZ_PER_TB a multiple of "
                 "NNZ_PER_WARP with <= 512 threads (got %lld, %lld, %lld)",
                 (long long)TB, (long long)W, (long long)TPT);
+  if (TPT == 4 || TPT == 8 || TPT == 16) return run_ttv_stream<T>(a, c, TB, (int)TPT);
   const TtvNnzLayout L = ttv_nnz_layout(a);
   if (!a.ws || a.ws_bytes < L.total) return fail(SPX_E_WORKSPACE, "workspace %zu < %zu bytes", a.ws_bytes, L.total);
   T* fsum = reinterpret_cast<T*>(static_cast<char*>(a.ws) + L.fsum);
@@ -767,7 +1005,10 @@ int run_ttv_nnz(const Args& a) {
 }  // namespace
 
 size_t ws_csf(int kid, const Args& a) {
-  if (kid == SPX_K_TTV_NNZ) return ttv_nnz_layout(a).total;
+  if (kid == SPX_K_TTV_NNZ) {
+    const int tpt = a.params[2];
+    return (tpt == 4 || tpt == 8 || tpt == 16) ? 0 : ttv_nnz_layout(a).total;  // the streaming form needs none
+  }
   if (kid != SPX_K_MTTKRP_NNZ) return 0;
   const int64_t nnz = a.level_sizes[2];
   const int64_t W = a.params[1] > 0 ? a.params[1] : 1;

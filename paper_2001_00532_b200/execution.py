@@ -36,6 +36,27 @@ def _cur_stream(device) -> int:
     return torch.cuda.current_stream(device).cuda_stream
 
 
+# The kernels move dense rows with 256-bit / 128-bit vector accesses and
+# stream crd/vals with 16 B loads; a view with an arbitrary storage offset
+# (x[1:], a column slice made contiguous at an odd element) would fault with
+# a misaligned address.  Such operands are copied into a fresh allocation
+# (256 B aligned) before launch; an unaligned output is computed into an
+# aligned buffer and copied back after each launch.
+ALIGN = 32
+
+
+def _aligned(t: torch.Tensor) -> torch.Tensor:
+    return t if t.data_ptr() % ALIGN == 0 else t.clone()
+
+
+def _aligned_operand(d: DeviceTensor) -> DeviceTensor:
+    arrays = list(d.pos.values()) + list(d.crd.values()) + [d.vals]
+    if all(a.data_ptr() % ALIGN == 0 for a in arrays):
+        return d
+    return DeviceTensor(dims=d.dims, levels=d.levels, pos={k: _aligned(v) for k, v in d.pos.items()},
+                        crd={k: _aligned(v) for k, v in d.crd.items()}, vals=_aligned(d.vals))
+
+
 class Executor:
     """A Program bound to device operands and an output buffer.
 
@@ -49,8 +70,10 @@ class Executor:
                  dense_out: bool | None = None):
         self.program = program
         self.dtype = dtype
+        operands = {k: _aligned_operand(v) for k, v in operands.items()}
         self.operands = operands
         self.out = out
+        self._dev_out = out if out.data_ptr() % ALIGN == 0 else torch.empty_like(out)
         lib = _lib.load()
         order = program.tensor_order
         sp = operands[program.ec.tensors[0]]
@@ -70,6 +93,7 @@ class Executor:
             self.plan.params[7] = 1 if dense_out else 0
         ws = lib.spx_workspace_size(ctypes.byref(self.plan), self._dims)
         self.workspace = torch.empty(max(int(ws), 1), dtype=torch.uint8, device=out.device)
+        self._ws_ptr = ctypes.c_void_p(self.workspace.data_ptr())
         self.ws_bytes = int(ws)
         self._lib = lib
 
@@ -77,16 +101,19 @@ class Executor:
         s = stream if stream is not None else _cur_stream(self.out.device)
         st = self._lib.spx_launch(
             ctypes.byref(self.plan),
-            ctypes.c_void_p(self.out.data_ptr()),
+            ctypes.c_void_p(self._dev_out.data_ptr()),
             self._vals,
             self._pos,
             self._crd,
             self._dims,
-            ctypes.c_void_p(self.workspace.data_ptr()),
+            self._ws_ptr,
             ctypes.c_size_t(self.ws_bytes),
             ctypes.c_void_p(s),
         )
         _lib.check(st, f"spx_launch[{self.program.kernel}]")
+        if self._dev_out is not self.out:
+            with torch.cuda.stream(torch.cuda.ExternalStream(s, device=self.out.device)):
+                self.out.copy_(self._dev_out)
 
     def capture(self, repeat: int = 1) -> "torch.cuda.CUDAGraph":
         """Capture `repeat` launches into a CUDA graph; `g.replay()` then
@@ -105,6 +132,11 @@ class Executor:
 
     def stats(self) -> "ExecStats":
         return ExecStats(self.program, self.plan, self.sparse, self.dims_map)
+
+    def manifest(self):
+        """The reference `ir.Manifest` of this launch (the Program is not
+        modified by binding: each Executor carries its own dims)."""
+        return self.program.manifest(self.dims_map)
 
 
 def _infer_dtype(inputs: dict) -> str:
@@ -192,8 +224,6 @@ def interpret(program: Program, inputs: dict, out_dims=None, *, dtype: str | Non
     device = torch.device(device or "cuda")
     dtype = dtype or _infer_dtype(inputs)
     dims = _check_extents(program, inputs)
-    if program.dims is None:
-        program.dims = dims
     ops = {}
     fmt = _spindle.tensors.format_shorthand
     for t in program.tensor_order:
@@ -283,6 +313,10 @@ class ExecStats:
         self.params = [int(plan.params[k]) for k in range(8)]
         self._sparse = sparse
         self._dims = dims
+
+    def manifest(self):
+        """The `ir.Manifest` (parameter layout + dims) of this execution."""
+        return self.program.manifest(self._dims)
 
     def _pos(self, lvl: int) -> np.ndarray:
         return self._sparse.pos[lvl].cpu().numpy()

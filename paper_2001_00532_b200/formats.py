@@ -144,11 +144,6 @@ class DeviceTensor:
         t.vals = self.vals.cpu().numpy().astype(np.float64)
         return t
 
-    def to_dense_array(self) -> np.ndarray:
-        if self.is_dense:
-            return self.vals.cpu().numpy().reshape(self.dims).astype(np.float64)
-        return self.to_reference().to_dense()
-
 
 def as_device_operand(x, levels: str | None, device, dtype: str) -> DeviceTensor:
     """Coerce an `interpret` input (reference Tensor / DenseTensor / ndarray /

@@ -303,8 +303,69 @@ def _function(src: str, name: str):
     return fn
 
 
+def _static_extent(prov, name: str, ext: dict, level_nnz: dict, memo: dict):
+    """Runtime extent of a provenance variable when it does not vary per
+    segment (SPEC.md:355 propagate_bounds rules): original coordinate
+    variables, split / divide / bound / coordinate fuse of those, and a
+    position variable over a whole compressed level (pos cut from the
+    root: [0, nnz of that level)).  None when it is per-segment."""
+    if name in memo:
+        return memo[name]
+    S = _spindle.schedule
+    rel = prov.producing(name)
+    e = None
+    if rel is None:
+        e = ext.get(name)
+    elif isinstance(rel, S.SplitRel):
+        p = _static_extent(prov, rel.parent, ext, level_nnz, memo)
+        e = rel.inner_size if name == rel.inner else (None if p is None else -(-p // rel.inner_size))
+    elif isinstance(rel, S.DivideRel):
+        p = _static_extent(prov, rel.parent, ext, level_nnz, memo)
+        e = rel.outer_size if name == rel.outer else (None if p is None else -(-p // rel.outer_size))
+    elif isinstance(rel, S.BoundRel):
+        e = rel.bound
+    elif isinstance(rel, S.FuseRel):
+        a = _static_extent(prov, rel.left, ext, level_nnz, memo)
+        b = _static_extent(prov, rel.right, ext, level_nnz, memo)
+        if a is not None and b is not None and prov.pos_info(rel.left) is None and prov.pos_info(rel.right) is None:
+            e = a * b
+    elif isinstance(rel, S.PosRel):
+        if rel.covered and rel.covered[0] == 0:
+            e = level_nnz.get((rel.access.tensor, rel.level))
+    memo[name] = e
+    return e
+
+
+def check_bounds(prog: "GenericProgram", ops: dict) -> None:
+    """MaxExact contract (`AssertExtent` ir.py:208-212):
+    every `bound(src, dst, c, MaxExact)` whose source has a static runtime
+    extent must see exactly c, else ContractViolation -- the same check the
+    table kernels make at launch (spx_launch -> SPX_E_CONTRACT)."""
+    E = _spindle.errors
+    S = _spindle.schedule
+    ext = {}
+    for acc in prog.stmt.assignment.input_accesses():
+        for v, d in zip(acc.vars, ops[acc.tensor].dims):
+            ext.setdefault(v.name, int(d))
+    level_nnz = {}
+    for t in prog.tensor_order:
+        for lvl, n in enumerate(ops[t].level_sizes()):
+            level_nnz[(t, lvl)] = int(n)
+    prov = prog.stmt.provenance
+    memo: dict = {}
+    for v in prov.nodes:
+        rel = prov.producing(v.name)
+        if isinstance(rel, S.BoundRel):
+            e = _static_extent(prov, rel.source, ext, level_nnz, memo)
+            if e is not None and e != rel.bound:
+                raise E.ContractViolation(
+                    f"MaxExact bound violated: bound({rel.source}, {rel.bounded}, {rel.bound}) but the runtime "
+                    f"extent of {rel.source} is {e}")
+
+
 def launch(prog: GenericProgram, ops: dict, out: torch.Tensor, dtype: str, stream: int) -> dict:
     """Zero `out` and run every term kernel; returns work counts."""
+    check_bounds(prog, ops)
     g = _Gen(prog.stmt, {t: ops[t].dims for t in prog.tensor_order}, dtype)
     src, terms = g.source()
     out.zero_()

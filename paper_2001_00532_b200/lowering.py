@@ -439,7 +439,7 @@ def _match_spmv(sh: _Shape) -> Program:
         # K2 warp-per-row (A.8): pos(j) split into thread_nz (outer) x thread (inner, 32 lanes)
         b2, s2 = _unify(jg, [("thread_nz", [("so", "L")]), ("thread", [("si", "L")])])
         if s2["L"] != 32:
-            raise _err().LoweringError("warp-per-row SpMV needs the position split size WARP_SIZE=32")
+            raise _NoMatch  # the warp-per-row kernel maps the position split onto 32 lanes
         kv = {"block": rows.get("block"), "warp": rows.get("warp"), "thread": b2["thread"]}
         R, Wn = rp
         return Program(sh.stmt, ec, _lib.K_SPMV_WARP, [R or 8, Wn or min(R or 8, 8)], row_divide=div, vars=kv)
@@ -531,6 +531,37 @@ def _match_mttkrp(sh: _Shape) -> Program:
     raise _NoMatch
 
 
+_MAX_WARPS = 16  # kMaxWarps (csrc/spx_common.cuh)
+_MAX_THREADS = 512  # kMaxThreads
+
+
+def _check_launchable(prog: Program) -> None:
+    """The launch-time constraints of each table kernel (the checks
+    spx_launch makes before it launches, csrc/spx_{spmv,spmm,sddmm,csf}.cu),
+    applied at lower() time: a schedule whose constants a kernel cannot run
+    is not a match for it (raise _NoMatch -> generic lowering or
+    LoweringError), instead of failing later inside interpret()."""
+    kid, p = prog.kernel_id, list(prog.params) + [0] * 8
+    if kid in (_lib.K_SPMM_NNZ, _lib.K_SDDMM_NNZ, _lib.K_MTTKRP_NNZ):
+        TB, W = p[0], p[1]
+        if TB < 1 or W < 1 or TB % W or TB // W > _MAX_WARPS:
+            raise _NoMatch
+    if kid in (_lib.K_SPMV_NNZ, _lib.K_TTV_NNZ):
+        TB, W, T = p[0], p[1], p[2]
+        if TB < 1 or W < 1 or T < 1 or W != 32 * T or TB % W or TB // T > _MAX_THREADS:
+            raise _NoMatch
+    if kid in (_lib.K_SPMM_NNZ, _lib.K_SPMM_ROW, _lib.K_SDDMM_NNZ, _lib.K_SDDMM_ROW, _lib.K_MTTKRP_NNZ):
+        if p[2] not in (0, 32):  # the lanes split of the dense dimension
+            raise _NoMatch
+    if kid == _lib.K_TTV_FIBER:
+        FTB, FW = p[0] or 256, p[1] or 32
+        if -(-FTB // FW) > _MAX_WARPS:
+            raise _NoMatch
+    if kid in (_lib.K_SPMV_WARP, _lib.K_SPMM_ROW, _lib.K_SDDMM_ROW, _lib.K_MTTKRP_SLICE, _lib.K_SPMV_ROW):
+        if any(x < 0 for x in p[:2]):
+            raise _NoMatch
+
+
 def lower(stmt, formats=None, dims=None, *, fallback: bool = True):
     """Select the sm_100a kernel for a scheduled statement.
 
@@ -574,6 +605,7 @@ def _lower_table(stmt, formats=None, dims=None) -> Program:
             prog = _match_ttv(sh)
         else:
             prog = _match_mttkrp(sh)
+        _check_launchable(prog)
     except _NoMatch:
         raise E.LoweringError(
             f"no kernel in the selection table matches the {ec.kind} schedule shape {sh.text()}"

@@ -77,3 +77,35 @@ def test_generic_uses_the_gpu(cuda):
     before = _lib.launch_count()
     interpret(lower(stmt), {"A": A, "x": rng.uniform(-1, 1, 40)})
     assert _lib.launch_count() > before  # spx_jit_launch counted
+
+
+def test_generic_maxexact_violation_raises(cuda):
+    """a MaxExact bound outside every table template reaches the
+    generic lowering, which must still check it."""
+    asg = N.parse_assignment("y(i) = A(i,j) * x(j)")
+    stmt = S.concretize(asg, {"A": "ds", "x": "d"})
+    stmt = S.apply_schedule(stmt, "split(i, i0, i1, 8)\nbound(i0, ib, 2, MaxExact)")
+    prog = lower(stmt)
+    assert prog.kind == "generic"
+    rng = np.random.default_rng(0)
+    A, Ad = _rand_tensor((24, 10), "ds", rng)  # ceil(24/8) = 3 != 2
+    x = rng.uniform(-1, 1, 10)
+    with pytest.raises(_spindle.errors.ContractViolation):
+        interpret(prog, {"A": A, "x": x})
+    A, Ad = _rand_tensor((16, 10), "ds", rng)  # ceil(16/8) = 2: holds
+    res, _ = interpret(prog, {"A": A, "x": x})
+    assert rel_err(res.data, Ad @ x) <= 1e-12
+
+
+@pytest.mark.parametrize("entry,params", [("A4", {"WARP_SIZE": 16, "BOUND": 8}),
+                                          ("A4", {"NNZ_PER_TB": 1000, "NNZ_PER_WARP": 64})])
+def test_unlaunchable_table_constants_run_generic(cuda, entry, params):
+    from paper_2001_00532_b200 import corpus
+
+    prog = lower(corpus.build(entry, **params))
+    assert prog.kind == "generic"
+    rng = np.random.default_rng(1)
+    A, Ad = _rand_tensor((30, 20), "ds", rng)
+    B = rng.uniform(-1, 1, (20, 128))
+    res, _ = interpret(prog, {"A": A, "B": B})
+    assert rel_err(res.data, Ad @ B) <= 1e-12

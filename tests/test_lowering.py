@@ -144,3 +144,27 @@ def test_dense_sparse_operand_formats_checked():
     stmt = S.concretize(N.parse_assignment(corpus.SPMV), {"A": "ss", "x": "d"})
     with pytest.raises(E.LoweringError):
         lower(stmt, fallback=False)
+
+
+# -- launch-time constraints are checked at lower() time ----------
+
+
+@pytest.mark.parametrize("entry,params", [
+    ("A4", {"WARP_SIZE": 16, "BOUND": 8}),               # dense lanes must be 32
+    ("A4", {"NNZ_PER_TB": 1000, "NNZ_PER_WARP": 64}),     # TB % W != 0
+    ("A4", {"NNZ_PER_TB": 64 * 32, "NNZ_PER_WARP": 64}),  # 32 warps per CTA > 16
+    ("A2", {"NNZ_PER_TB": 2048, "NNZ_PER_WARP": 128, "NNZ_PER_THREAD": 8}),  # W != 32*T
+    ("A6", {"WARP_SIZE": 16, "BOUND": 2}),
+    ("K6", {"NNZ_PER_TB": 96, "NNZ_PER_WARP": 64}),
+])
+def test_unlaunchable_constants_do_not_select_a_table_kernel(entry, params):
+    stmt = corpus.build(entry, **params)
+    with pytest.raises(E.LoweringError):
+        lower(stmt, fallback=False)
+    prog = lower(stmt)  # the generic lowering takes it instead
+    assert prog.kind == "generic"
+
+
+def test_launchable_constants_still_select_the_table():
+    assert lower(corpus.build("A4", NNZ_PER_TB=512 * 16, NNZ_PER_WARP=512)).kernel == "spmm_nnz"
+    assert lower(corpus.build("A2", NNZ_PER_TB=512 * 4, NNZ_PER_WARP=128, NNZ_PER_THREAD=4)).kernel == "spmv_nnz"
