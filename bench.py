@@ -187,6 +187,9 @@ def reference_dense_eval_cfg1():
                       f"{s:.3f} s", "oracle_rel_err": err}
 
 
+_AFFINITY = len(os.sched_getaffinity(0))  # read before OpenMP binds the main thread (OMP_PROC_BIND)
+
+
 def host_cpu_info():
     try:
         model = next(ln.split(":", 1)[1].strip() for ln in open("/proc/cpuinfo") if ln.startswith("model name"))
@@ -196,7 +199,7 @@ def host_cpu_info():
         smt = Path("/sys/devices/system/cpu/smt/active").read_text().strip() == "1"
     except Exception:
         smt = None
-    return {"model": model, "threads": len(os.sched_getaffinity(0)), "smt": smt}
+    return {"model": model, "threads": _AFFINITY, "smt": smt}
 
 
 def cached_config(cfg: int, rank: int, world: int, dist=None):

@@ -106,7 +106,8 @@ def load(path: str | os.PathLike | None = None):
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    # SPX_LIB: a tuning variant built by build.build_variant (tools only)
+    p = Path(path) if path else Path(os.environ.get("SPX_LIB") or LIB_PATH)
     if not p.exists():
         raise RuntimeError(
             f"{p} is missing: the CUDA backend is not built "

@@ -89,6 +89,28 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     return LIB
 
 
+def build_variant(tag: str, src_name: str, defines: list[str]) -> Path:
+    """Tuning tool: libspx with one source recompiled under extra -D flags,
+    linked from the regular objects into tools/variants/libspx_<tag>.so
+    (load it with SPX_LIB=<path>; the product always loads libspx.so)."""
+    build()
+    out_dir = ROOT / "tools" / "variants"
+    out_dir.mkdir(exist_ok=True)
+    obj = out_dir / f"{Path(src_name).stem}_{tag}.o"
+    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *defines, "-c", str(CSRC / src_name), "-o", str(obj)]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"nvcc failed for {src_name} ({tag}):\n{res.stderr}")
+    objs = [obj if o.stem == Path(src_name).stem else o for o in (OBJ / (s.stem + ".o") for s in _sources())]
+    lib = out_dir / f"libspx_{tag}.so"
+    res = subprocess.run([nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", str(lib), *map(str, objs)],
+                         capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"link failed:\n{res.stderr}")
+    obj.unlink()
+    return lib
+
+
 REF_SRC = Path("/root/reference/pkg")
 REF_DST = ROOT / "baseline" / "_ref"
 

@@ -174,7 +174,7 @@ reorder(block, warp, thread, thread_nz)
 parallelize(block, GPUBlock, IgnoreRaces)
 parallelize(warp, GPUWarp, IgnoreRaces)
 parallelize(thread, GPUThread, Atomics)""",
-          {"NNZ_PER_TB": 2048, "NNZ_PER_WARP": 256, "NNZ_PER_THREAD": 8}, "ttv_nnz"),
+          {"NNZ_PER_TB": 8192, "NNZ_PER_WARP": 512, "NNZ_PER_THREAD": 16}, "ttv_nnz"),
     Entry("K9", "slice-split MTTKRP on GPU (row a20 K9, A.5 shape)", MTTKRP, F_MTTKRP,
           """pos(i, ipos, B(i,k,l))
 split(ipos, block, warp, {SLICES_PER_TB})

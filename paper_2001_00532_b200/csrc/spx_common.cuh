@@ -237,6 +237,16 @@ __device__ __forceinline__ void ld256_nc_hint(const double* p, double* r, uint64
                : "l"(p), "l"(pol));
 }
 
+// cp.async.bulk.prefetch.L2: pull [p, p + bytes) into L2 (bytes % 16 == 0, p 16 B aligned)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void ld256_i32_hint(const int32_t* p, int* r, uint64_t pol) {
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.s32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "l"(p), "l"(pol));
+}
+
 #ifndef SPX_FRAG_LD256
 #define SPX_FRAG_LD256 1
 #endif

@@ -720,196 +720,230 @@ __global__ void ttv_scatter_kernel(const int32_t* __restrict__ crd0, const int32
 // ---------------------------------------------------------------------------
 // K11 TTV nnz-split, streaming form.  The leaf level is a CSR whose rows are
 // the fibers (pos2 the row pointer); A(i,j) = sum_k B(i,j,k) c(k) is a
-// segmented sum over the leaf stream, and the stream is the only HBM-sized
-// traffic (8 B per fp32 leaf: crd2 + vals), so the kernel is built to keep
-// that stream moving:
-//  * the schedule's block (NNZ_PER_TB leaves) is a tile; a persistent CTA
-//    takes a contiguous run of tiles, so the fiber open at the next tile's
-//    first leaf (and its slice) falls out of the current tile's setup -- no
-//    search per tile, no chunk table, no extra launch;
-//  * a thread (NNZ_PER_THREAD = LPT leaves) loads its coordinates and values
-//    with 16 B vector loads before the tile setup runs (the loads are in
-//    flight meanwhile), c is staged in shared memory;
-//  * tile setup: the fibers starting inside the tile (pos2 in (p0, p1)),
-//    compacted to the non-empty ones, with their output offsets
-//    crd0[slice]*J + crd1[f] (slice tracked from the previous one: "step:
-//    while-advance over pos boundaries"), go to shared memory;
-//  * a thread folds its leaves fiber by fiber (Track recovery: the next
-//    fiber start is compared against the position), stores fibers that
-//    start and end inside it, and a segmented warp scan joins the partials
-//    that cross lanes; fibers crossing a warp boundary are completed with
-//    one red.add per warp end (the schedule's Atomics strategy on the
-//    thread loop; A is zeroed first).
+// segmented sum over the leaf stream, and that stream (crd2 + vals, 8 B per
+// fp32 leaf) is the only HBM-sized traffic, so the kernel is built to keep
+// it moving with no block-wide synchronisation:
+//  * the schedule's warp split (NNZ_PER_WARP = 32 * NNZ_PER_THREAD leaves) is
+//    a chunk; a warp takes chunks grid-stride, a CTA's warps the NNZ_PER_TB
+//    consecutive leaves of one block instance per round;
+//  * a pre-pass (one launch, fully parallel, no searches) zeroes A and builds
+//    the chunk table: the fiber holding each chunk's first leaf (a scatter
+//    over fibers) and its slice (a scatter over slices) -- SearchSegment
+//    (ir.py:178-190) for every chunk start without a dependent search;
+//  * per chunk, a lane issues its NNZ_PER_THREAD coordinates and values as
+//    16 B vector loads first; the fibers starting inside the chunk come from
+//    one coalesced window of pos2 / crd1 (their slices advance from the
+//    chunk's slice: "step: while-advance over pos boundaries")
+//    and are marked in a per-warp head mask with their output offsets
+//    crd0[slice]*J + crd1[f]; the next chunk's table entry is prefetched;
+//  * a lane folds its leaves fiber by fiber, stores fibers that start and
+//    end inside it, and one segmented warp scan joins the partials crossing
+//    lanes; a fiber crossing a chunk boundary gets one red.add per chunk end
+//    (the schedule's Atomics strategy on the thread loop; A zeroed first).
 // ---------------------------------------------------------------------------
+template <typename T>
+__global__ void ttv_prep_kernel(const int32_t* __restrict__ pos1, const int32_t* __restrict__ pos2,
+                                int32_t* __restrict__ chunkF, int32_t* __restrict__ chunkS, T* __restrict__ A,
+                                int64_t nA, int S, int F, int CH) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, gs = (int64_t)gridDim.x * blockDim.x;
+  float4* A4 = reinterpret_cast<float4*>(A);
+  const int64_t n4 = nA * (int64_t)sizeof(T) / 16;
+  for (int64_t i = g; i < n4; i += gs) A4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int64_t i = n4 * 16 / (int64_t)sizeof(T) + g; i < nA; i += gs) A[i] = T(0);
+  // chunk starts inside fiber f (non-empty: [pos2[f], pos2[f+1])) -> chunkF;
+  // eight fibers per thread, their nine pos2 entries loaded together
+  for (int64_t f0 = g * 8; f0 < F; f0 += gs * 8) {
+    int p[9];
+#pragma unroll
+    for (int u = 0; u < 9; ++u) p[u] = __ldg(pos2 + min(f0 + u, (int64_t)F));
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      for (int t = (p[u] + CH - 1) / CH; (int64_t)t * CH < p[u + 1]; ++t) chunkF[t] = (int)(f0 + u);
+  }
+  // chunk starts inside slice s (leaves [pos2[pos1[s]], pos2[pos1[s+1]])) -> chunkS;
+  // one warp per slice, lanes over its chunks (a heavy slice holds thousands)
+  const int lane = threadIdx.x & 31;
+  for (int64_t s = g >> 5; s < S; s += gs >> 5) {
+    const int a = __ldg(pos2 + __ldg(pos1 + s)), b = __ldg(pos2 + __ldg(pos1 + s + 1));
+    for (int t = (a + CH - 1) / CH + lane; (int64_t)t * CH < b; t += 32) chunkS[t] = (int)s;
+  }
+}
+
+// c staged in shared memory at a hashed position: the bit-skewed mode
+// indices of real tensors (cfg4: P(bit)=0.3) concentrate on low-popcount
+// values -- 0, 32, 64, ..., 1024 all share bank 0 in a plain layout.  The
+// low five bits are XORed with a multiplicative hash of the rest (a
+// permutation inside every 32-entry block).
+__device__ __forceinline__ int c_slot(int k) { return k ^ (int)(((unsigned)(k >> 5) * 0x9E3779B1u) >> 27); }
+
+__device__ __forceinline__ int ld_i32_early(const int32_t* p) {
+  int r;  // volatile: issued where written (a prefetch for the next loop trip), not sunk to its use
+  asm volatile("ld.global.nc.b32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
+
+#ifndef SPX_TTV_PREFETCH
+#define SPX_TTV_PREFETCH 0
+#endif
+#ifdef SPX_TTV_MAXNREG
+#define SPX_TTV_BOUNDS __maxnreg__(SPX_TTV_MAXNREG)
+#else
+#define SPX_TTV_BOUNDS __launch_bounds__(512)
+#endif
 template <typename T, int LPT, typename OffT>
-__global__ void __launch_bounds__(512) ttv_stream_kernel(
+__global__ void SPX_TTV_BOUNDS ttv_stream_kernel(
     const int32_t* __restrict__ crd0, const int32_t* __restrict__ pos1, const int32_t* __restrict__ crd1,
     const int32_t* __restrict__ pos2, const int32_t* __restrict__ crd2, const T* __restrict__ vals,
-    const T* __restrict__ c, T* __restrict__ A, int S, int F, int nnz, int64_t J, int K, int TB, int ntiles,
-    int csmem) {
-  static_assert(LPT % 4 == 0 && LPT <= 16, "whole 16 B coordinate vectors per thread");
-  constexpr int VCH = LPT * (int)sizeof(T) / 16;  // 16 B value vectors per thread
-  constexpr int VPC = 16 / (int)sizeof(T);
+    const T* __restrict__ c, const int32_t* __restrict__ chunkF, const int32_t* __restrict__ chunkS,
+    T* __restrict__ A, int S, int F, int nnz, int64_t J, int K, int nchunks, int csmem) {
+  static_assert(LPT % 4 == 0 && LPT <= 16, "rows of 4 or 8 leaves per lane");
+  constexpr int CH = 32 * LPT;          // leaves per warp chunk
+  constexpr int RL = LPT >= 8 ? 8 : 4;  // consecutive leaves per lane in a row
+  constexpr int ROWS = LPT / RL;        // a chunk is ROWS rows of 32*RL leaves
+  constexpr int RW = 32 * RL;           // leaves per row
+  constexpr int RMASK = (1 << RL) - 1;
   extern __shared__ __align__(16) unsigned char sm[];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x;
-  // layout: starts[TB] | offs[TB] | c[K] (when staged)
-  int* starts = reinterpret_cast<int*>(sm);
-  OffT* offs = reinterpret_cast<OffT*>(sm + (size_t)TB * 4);
-  T* sc = reinterpret_cast<T*>(sm + (size_t)TB * 4 + (size_t)TB * sizeof(OffT));
-  __shared__ int s_warp_cnt[kMaxWarps + 1];
-  __shared__ int s_nf, s_fnext, s_snext;
-  __shared__ OffT s_off_in;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, wpc = blockDim.x >> 5;
+  // layout: per warp { offp[CH] (OffT), mask[32] } | c[K] (when staged)
+  constexpr int kWarpBytes = CH * (int)sizeof(OffT) + 32 * 4;
+  OffT* offp = reinterpret_cast<OffT*>(sm + (size_t)warp * kWarpBytes);
+  unsigned* mask = reinterpret_cast<unsigned*>(sm + (size_t)warp * kWarpBytes + CH * sizeof(OffT));
+  T* sc = reinterpret_cast<T*>(sm + (size_t)wpc * kWarpBytes);
   if (csmem) {
-    for (int k = tid; k < K; k += nthr) sc[k] = __ldg(c + k);
+    for (int k = threadIdx.x; k < K; k += blockDim.x) sc[c_slot(k)] = __ldg(c + k);
+    __syncthreads();
   }
-  // this CTA's contiguous tile range
-  const int t_begin = (int)(((int64_t)ntiles * blockIdx.x) / gridDim.x);
-  const int t_end = (int)(((int64_t)ntiles * (blockIdx.x + 1)) / gridDim.x);
-  if (t_begin >= t_end) return;
-  // fiber and slice open at the first tile's first leaf (SearchSegment, ir.py:178-190)
-  if (warp == 0) {
-    const int f = (int)warp_search_segment(pos2, 0, F, (int64_t)t_begin * TB, lane);
-    const int s = (int)warp_search_segment(pos1, 0, S, f, lane);
-    if (lane == 0) {
-      s_fnext = f;
-      s_snext = s;
-    }
-  }
-  __syncthreads();
   const uint64_t pol = l2_evict_first();
-  for (int t = t_begin; t < t_end; ++t) {
-    const int p0 = t * TB;
-    const int p1 = min(p0 + TB, nnz);
-    const int f_lo = s_fnext, s_lo = s_snext;
-    // -- the thread's leaves: issue the loads first ------------------------
-    const int q0 = p0 + tid * LPT;
+  const unsigned lt = (1u << lane) - 1u;  // lanes below mine
+  const int stride = gridDim.x * wpc;
+  int chunk = blockIdx.x * wpc + warp;
+  int fi = chunk < nchunks ? __ldg(chunkF + chunk) : 0, si = chunk < nchunks ? __ldg(chunkS + chunk) : 0;
+  for (; chunk < nchunks; chunk += stride) {
+    const int p0 = chunk * CH, p1 = min(p0 + CH, nnz);
+    // the first window of fibers that may start in the chunk and the chunk's
+    // slice: one L2 round trip, issued first
+    int f = fi + 1 + lane;
+    int q = f < F ? __ldg(pos2 + f) : INT_MAX;
+    int qn = f < F ? __ldg(pos2 + f + 1) : INT_MAX;
+    int kf = f < F ? __ldg(crd1 + f) : 0;
+    const int i_in = __ldg(crd0 + si), send_in = __ldg(pos1 + si + 1);
+    const OffT off_in = (OffT)i_in * (OffT)J + (OffT)__ldg(crd1 + fi);
+    // the next chunk's table entry (issued now, used next trip)
+    const int nxt = min(chunk + stride, nchunks - 1);
+    const int fi_n = ld_i32_early(chunkF + nxt), si_n = ld_i32_early(chunkS + nxt);
+    // row h, lane L: leaves p0 + RW*h + RL*L + e (e < RL) -- every warp load
+    // is one coalesced run (32 B per lane for RL = 8)
     int kk[LPT];
     T v[LPT];
-    if (q0 + LPT <= p1) {
+    if (p0 + CH <= p1) {
 #pragma unroll
-      for (int h = 0; h < LPT / 4; ++h) {
-        const int4 k4 = ld_i4_hint(crd2 + q0 + 4 * h, pol);
-        kk[4 * h] = k4.x;
-        kk[4 * h + 1] = k4.y;
-        kk[4 * h + 2] = k4.z;
-        kk[4 * h + 3] = k4.w;
+      for (int h = 0; h < ROWS; ++h) {
+        const int qq = p0 + RW * h + RL * lane;
+        if constexpr (RL == 8) {
+          ld256_i32_hint(crd2 + qq, kk + 8 * h, pol);
+          ld256_nc_hint(vals + qq, v + 8 * h, pol);
+          if constexpr (sizeof(T) == 8) ld256_nc_hint(vals + qq + 4, v + 8 * h + 4, pol);
+        } else {
+          const int4 k4 = ld_i4_hint(crd2 + qq, pol);
+          kk[4 * h] = k4.x;
+          kk[4 * h + 1] = k4.y;
+          kk[4 * h + 2] = k4.z;
+          kk[4 * h + 3] = k4.w;
+          if constexpr (sizeof(T) == 4) unpack16<T>(v + 4 * h, ld_f4_hint(vals + qq, pol));
+          else ld256_nc_hint(vals + qq, v + 4 * h, pol);
+        }
       }
-#pragma unroll
-      for (int h = 0; h < VCH; ++h) unpack16<T>(v + h * VPC, ld_f4_hint(vals + q0 + h * VPC, pol));
     } else {
 #pragma unroll
       for (int j = 0; j < LPT; ++j) {
-        const bool in = q0 + j < p1;
-        kk[j] = in ? __ldg(crd2 + q0 + j) : 0;
-        v[j] = in ? __ldg(vals + q0 + j) : T(0);
+        const int qq = p0 + RW * (j / RL) + RL * lane + (j % RL);
+        const bool in = qq < p1;
+        kk[j] = in ? __ldg(crd2 + qq) : 0;
+        v[j] = in ? __ldg(vals + qq) : T(0);
       }
     }
-    // -- tile setup: non-empty fibers starting in (p0, p1), compacted --------
-    if (tid == 0) {
-      s_nf = 0;
-      s_off_in = (OffT)__ldg(crd0 + s_lo) * (OffT)J + (OffT)__ldg(crd1 + f_lo);
+    if (SPX_TTV_PREFETCH && lane == 0 && chunk + stride < nchunks) {
+      const int pn = nxt * CH, nb = min(CH, nnz - pn);
+      bulk_prefetch_l2(crd2 + pn, (uint32_t)(((nb * 4) + 15) & ~15));
+      bulk_prefetch_l2(vals + pn, (uint32_t)(((nb * (int)sizeof(T)) + 15) & ~15));
     }
-    __syncthreads();
-    int sl = s_lo;  // slice of this thread's candidate fiber (monotone over batches)
-    for (int base = f_lo + 1;; base += nthr) {
-      const int f = base + tid;
-      const int q = f < F ? __ldg(pos2 + f) : INT_MAX;
-      const int qn = f < F ? __ldg(pos2 + f + 1) : INT_MAX;
-      const bool le = q <= p1;  // starts at or before the next tile's first leaf
-      const bool take = q < p1 && qn > q;  // a non-empty fiber starting in the tile
-      int s = sl;
-      if (le && f < F) {
-        // slice of fiber f: the largest s with pos1[s] <= f, from the last one
-        if (__ldg(pos1 + s + 1) <= f) s = (int)search_segment(pos1, s + 1, S, f);
+    mask[lane] = 0u;
+    __syncwarp();
+    // non-empty fibers starting in (p0, p1) become heads: bit RL*h + e of lane L's word
+    while (true) {
+      if (q < p1 && qn > q) {
+        // output offset crd0[slice]*J + crd1[f]; the slice advances from the
+        // chunk's ("step: while-advance over pos boundaries")
+        int isl = i_in;
+        if (send_in <= f) isl = __ldg(crd0 + search_segment(pos1, si + 1, S, f));
+        const int d = q - p0;
+        offp[d] = (OffT)isl * (OffT)J + (OffT)kf;
+        atomicOr(mask + (d % RW) / RL, 1u << ((d / RW) * RL + d % RL));
       }
-      const unsigned bal = __ballot_sync(kFull, take);
-      if (lane == 0) s_warp_cnt[warp] = __popc(bal);
-      const int nle = __syncthreads_count(le);
-      if (tid == 0) {
-        int acc = s_nf;
-        for (int w = 0; w < (nthr >> 5); ++w) {
-          const int x = s_warp_cnt[w];
-          s_warp_cnt[w] = acc;
-          acc += x;
-        }
-        s_warp_cnt[kMaxWarps] = acc;
-      }
-      __syncthreads();
-      if (take) {
-        const int r = s_warp_cnt[warp] + __popc(bal & ((1u << lane) - 1u));
-        starts[r] = q;
-        offs[r] = (OffT)__ldg(crd0 + s) * (OffT)J + (OffT)__ldg(crd1 + f);
-      }
-      if (le && (tid == nle - 1) && f < F) {  // the last fiber starting <= p1: open at the next tile
-        s_fnext = f;
-        s_snext = s;
-      }
-      __syncthreads();
-      if (tid == 0) s_nf = s_warp_cnt[kMaxWarps];
-      if (nle < nthr) break;
-      sl = s;  // every candidate was <= p1: the next batch continues from here
+      if (__shfl_sync(kFull, q, 31) >= p1) break;
+      f += 32;  // more than 32 fibers start in this chunk: the next window
+      q = f < F ? __ldg(pos2 + f) : INT_MAX;
+      qn = f < F ? __ldg(pos2 + f + 1) : INT_MAX;
+      kf = f < F ? __ldg(crd1 + f) : 0;
     }
-    __syncthreads();
-    const int nf = s_nf;
-    const OffT off_in = s_off_in;
-    // -- fold ----------------------------------------------------------------
-    // r = the fiber (rank in starts[], -1 = the tile's incoming fiber) open
-    // just before my first leaf
-    // (strictly before q0: a fiber starting at q0 is a start at my j = 0)
-    int lo = 0, hi = nf;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (starts[mid] < q0) lo = mid + 1;
-      else hi = mid;
-    }
-    int r = lo - 1;
-    const int r_first = r;
-    int next = r + 1 < nf ? starts[r + 1] : INT_MAX;
-    T acc = T(0), lead = T(0);
-    bool seen = false, lead_empty = false;
+    __syncwarp();
+    const unsigned hball = mask[lane];
+    OffT open_off = off_in;  // fiber open at the end of the previous row
+    bool started = false;    // has a fiber started in this chunk yet (warp-uniform)
+    T carry = T(0);          // its partial so far in this chunk
 #pragma unroll
-    for (int j = 0; j < LPT; ++j) {
-      const T x = v[j] * (csmem ? sc[kk[j]] : __ldg(c + kk[j]));
-      if (q0 + j == next) {  // a fiber starts here (Track: advance to it)
-        if (!seen) {
-          lead = acc;
-          lead_empty = j == 0;
-          seen = true;
-        } else {
-          A[offs[r]] = acc;  // started and ended inside this thread
-        }
-        ++r;
-        next = r + 1 < nf ? starts[r + 1] : INT_MAX;
-        acc = T(0);
-      }
-      acc += x;
-    }
-    // -- warp: join the partials that cross lanes ----------------------------
-    // value leaving each lane: its open segment; a lane that saw a start
-    // begins a new scan segment
-    T sv = seen ? acc : lead + acc;
-    if (!seen) lead = acc;
-    const unsigned heads = __ballot_sync(kFull, seen);
-    const int seg = 31 - __clz((heads | 1u) & (0xffffffffu >> (31 - lane)));
+    for (int h = 0; h < ROWS; ++h) {
+      const unsigned hb = (hball >> (RL * h)) & RMASK;
+      const unsigned rowheads = __ballot_sync(kFull, hb != 0u);
+      // the fiber open before my first leaf of this row: the last head in a
+      // lower lane of the row, else the one open at the previous row's end
+      const int dlast = hb ? RW * h + RL * lane + (31 - __clz(hb)) : 0;
+      const unsigned below = rowheads & lt;
+      const int dsrc = __shfl_sync(kFull, dlast, below ? 31 - __clz(below) : 0);
+      OffT cur = below ? offp[dsrc] : open_off;
+      const OffT first_off = cur;
+      T acc = T(0), lead = T(0);
+      bool seen = false, lead_empty = false;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const T y = __shfl_up_sync(kFull, sv, o);
-      if (lane - o >= seg && lane >= o) sv += y;
+      for (int e = 0; e < RL; ++e) {
+        const int j = RL * h + e;
+        const T x = v[j] * (csmem ? sc[c_slot(kk[j])] : __ldg(c + kk[j]));
+        if ((hb >> e) & 1u) {  // a fiber starts here (Track: advance to it)
+          if (!seen) {
+            lead = acc;
+            lead_empty = e == 0;
+            seen = true;
+          } else {
+            A[cur] = acc;  // started and ended inside this lane's run
+          }
+          cur = offp[RW * h + RL * lane + e];
+          acc = T(0);
+        }
+        acc += x;
+      }
+      // segmented inclusive scan of the partial leaving each lane; the
+      // previous rows' open partial enters at lane 0
+      T sv = (lane == 0 && !seen) ? acc + carry : acc;
+      const int seg = 31 - __clz((rowheads | 1u) & (0xffffffffu >> (31 - lane)));
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const T y = __shfl_up_sync(kFull, sv, o);
+        if (lane - o >= seg) sv += y;
+      }
+      T in = __shfl_up_sync(kFull, sv, 1);  // open partial arriving at my first leaf
+      if (lane == 0) in = carry;
+      if (seen) {  // my first start closes the fiber open before it
+        if (started || below) A[first_off] = in + lead;  // it started inside this chunk
+        else if (!(h == 0 && lane == 0 && lead_empty)) atomicAdd(A + first_off, in + lead);
+      }
+      carry = __shfl_sync(kFull, sv, 31);
+      open_off = __shfl_sync(kFull, cur, 31);
+      started = started || rowheads != 0u;
     }
-    T in = __shfl_up_sync(kFull, sv, 1);  // open partial arriving at my first leaf
-    if (lane == 0) in = T(0);
-    if (seen) {
-      // my first start closes fiber r_first (it holds in + lead in this warp)
-      const bool started_here = (heads & ((1u << lane) - 1u)) != 0u;
-      const OffT o = r_first >= 0 ? offs[r_first] : off_in;
-      if (started_here) A[o] = in + lead;
-      else if (!(lane == 0 && lead_empty)) atomicAdd(A + o, in + lead);
-    }
-    if (lane == 31) {  // the fiber open at the warp's end continues past it
-      const OffT o = r >= 0 ? offs[r] : off_in;
-      atomicAdd(A + o, sv);
-    }
-    __syncthreads();  // starts/offs are rewritten by the next tile
+    if (lane == 0) atomicAdd(A + open_off, carry);  // the fiber open at the chunk's end continues past it
+    fi = fi_n;
+    si = si_n;
+    __syncwarp();
   }
 }
 
@@ -933,13 +967,29 @@ TtvNnzLayout ttv_nnz_layout(const Args& a) {
 
 template <typename T, int LPT, typename OffT>
 int launch_ttv_stream(const Args& a, const Csf& c, int64_t TB) {
-  const int64_t J = a.dims[0][1], K = a.dims[0][2];
+  const int64_t I = a.dims[0][0], J = a.dims[0][1], K = a.dims[0][2];
+  constexpr int CH = 32 * LPT;
   const int threads = (int)(TB / LPT);
+  const int wpc = threads / 32;
   const int csmem = (size_t)K * sizeof(T) <= 16384 ? 1 : 0;
-  const size_t smem = (size_t)TB * (4 + sizeof(OffT)) + (csmem ? (size_t)K * sizeof(T) : 0);
+  const size_t smem = (size_t)wpc * (CH * sizeof(OffT) + 128) + (csmem ? (size_t)K * sizeof(T) : 0);
+  const int64_t nchunks = ceil_div(c.nnz, CH);
+  const size_t need = (size_t)2 * nchunks * sizeof(int32_t);
+  if (!a.ws || a.ws_bytes < need) return fail(SPX_E_WORKSPACE, "workspace %zu < %zu bytes", a.ws_bytes, need);
+  int32_t* chunkF = static_cast<int32_t*>(a.ws);
+  int32_t* chunkS = chunkF + nchunks;
+  T* A = static_cast<T*>(a.out);
+  const int64_t nA = I * J;
+  const int64_t prep_work = std::max<int64_t>(std::max<int64_t>(ceil_div(c.F, 8), nA * (int64_t)sizeof(T) / 16),
+                                              c.S * 32);
+  const int64_t prep_grid = std::min<int64_t>(ceil_div(prep_work, 256), (int64_t)num_sms() * 8);
+  ttv_prep_kernel<T><<<(unsigned)prep_grid, 256, 0, a.stream>>>(c.pos1, c.pos2, chunkF, chunkS, A, nA, (int)c.S,
+                                                                 (int)c.F, CH);
+  count_launch();
+  if (int e = check_cuda(cudaGetLastError(), "ttv_prep_kernel")) return e;
   auto kern = ttv_stream_kernel<T, LPT, OffT>;
   static thread_local size_t attr_set = 0;
-  if (smem > 48 * 1024 && smem > attr_set) {
+  if (smem > 32 * 1024 && smem > attr_set) {
     if (int e = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                            "smem attribute"))
       return e;
@@ -948,11 +998,10 @@ int launch_ttv_stream(const Args& a, const Csf& c, int64_t TB) {
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
   if (per_sm < 1) per_sm = 1;
-  const int64_t ntiles = ceil_div(c.nnz, TB);
-  const int64_t grid = min((int64_t)num_sms() * per_sm, ntiles);
+  const int64_t grid = std::min<int64_t>((int64_t)num_sms() * per_sm, ceil_div(nchunks, wpc));
   kern<<<(unsigned)grid, (unsigned)threads, smem, a.stream>>>(
       c.crd0, c.pos1, c.crd1, c.pos2, c.crd2, static_cast<const T*>(a.vals[0]), static_cast<const T*>(a.vals[1]),
-      static_cast<T*>(a.out), (int)c.S, (int)c.F, (int)c.nnz, J, (int)K, (int)TB, (int)ntiles, csmem);
+      chunkF, chunkS, A, (int)c.S, (int)c.F, (int)c.nnz, J, (int)K, (int)nchunks, csmem);
   count_launch();
   return check_cuda(cudaGetLastError(), "ttv_stream_kernel");
 }
@@ -975,15 +1024,16 @@ int run_ttv_nnz(const Args& a) {
   const Csf c = csf_of(a);
   const int64_t I = a.dims[0][0], J = a.dims[0][1];
   T* A = static_cast<T*>(a.out);
+  const int64_t TB = a.params[0], W = a.params[1], TPT = a.params[2];
+  if (c.nnz > 0 && (TPT == 4 || TPT == 8 || TPT == 16) && W == 32 * TPT && TB % W == 0 && TB / TPT <= kMaxThreads)
+    return run_ttv_stream<T>(a, c, TB, (int)TPT);  // zeroes A itself
   if (int e = check_cuda(cudaMemsetAsync(A, 0, (size_t)(I * J) * sizeof(T), a.stream), "memset")) return e;
   if (c.nnz == 0) return SPX_OK;
-  const int64_t TB = a.params[0], W = a.params[1], TPT = a.params[2];
   if (TB < 1 || W < 1 || TPT < 1 || W != 32 * TPT || TB % W != 0 || TB / TPT > kMaxThreads)
     return fail(SPX_E_UNSUPPORTED,
                 "TTV nnz-split needs NNZ_PER_WARP == 32*NNZ_PER_THREAD and NNZ_PER_TB a multiple of "
                 "NNZ_PER_WARP with <= 512 threads (got %lld, %lld, %lld)",
                 (long long)TB, (long long)W, (long long)TPT);
-  if (TPT == 4 || TPT == 8 || TPT == 16) return run_ttv_stream<T>(a, c, TB, (int)TPT);
   const TtvNnzLayout L = ttv_nnz_layout(a);
   if (!a.ws || a.ws_bytes < L.total) return fail(SPX_E_WORKSPACE, "workspace %zu < %zu bytes", a.ws_bytes, L.total);
   T* fsum = reinterpret_cast<T*>(static_cast<char*>(a.ws) + L.fsum);
@@ -1007,7 +1057,9 @@ int run_ttv_nnz(const Args& a) {
 size_t ws_csf(int kid, const Args& a) {
   if (kid == SPX_K_TTV_NNZ) {
     const int tpt = a.params[2];
-    return (tpt == 4 || tpt == 8 || tpt == 16) ? 0 : ttv_nnz_layout(a).total;  // the streaming form needs none
+    if (tpt == 4 || tpt == 8 || tpt == 16)  // the streaming form: the chunk table (fiber, slice)
+      return (size_t)2 * (size_t)ceil_div(a.level_sizes[2] > 0 ? a.level_sizes[2] : 1, 32 * tpt) * sizeof(int32_t);
+    return ttv_nnz_layout(a).total;
   }
   if (kid != SPX_K_MTTKRP_NNZ) return 0;
   const int64_t nnz = a.level_sizes[2];

@@ -197,7 +197,11 @@ def main():
         elif cfg == 3:
             run_sddmm(3, M, [("K6", {"BOUND": 8}), ("K10", {})], args)
         elif cfg == 4:
-            run_csf(4, M, {"mttkrp": [("A6", {}), ("K9", {}), ("MTTKRP0", {})], "ttv": [("K7", {}), ("K11", {})]}, args)
+            run_csf(4, M, {"mttkrp": [("A6", {}), ("K9", {}), ("MTTKRP0", {})], "ttv": [("K7", {}), ("K11", {}),
+                                ("K11", {"NNZ_PER_TB": 4096, "NNZ_PER_WARP": 512, "NNZ_PER_THREAD": 16}),
+                                ("K11", {"NNZ_PER_TB": 8192, "NNZ_PER_WARP": 512, "NNZ_PER_THREAD": 16}),
+                                ("K11", {"NNZ_PER_TB": 2048, "NNZ_PER_WARP": 512, "NNZ_PER_THREAD": 16}),
+                                ("K11", {"NNZ_PER_TB": 1024, "NNZ_PER_WARP": 128, "NNZ_PER_THREAD": 4})]}, args)
         del M
         torch.cuda.empty_cache()
 
