@@ -531,6 +531,227 @@ __device__ __forceinline__ void mttkrp_walk(const MttkrpCtx<T, VPL, CONTIG>& c, 
 }
 #undef SPX_DROW
 
+// ---------------------------------------------------------------------------
+// K8 for rank-32 fp32 (the cfg4 shape): quarter-warp sub-chunks.
+//
+// The warp's chunk of NNZ_PER_WARP leaves is cut into four contiguous
+// quarter chunks; quarter qw (8 lanes x float4 = one 128 B row) walks its
+// own leaves with its own fiber / slice state.  A group of four leaves that
+// stays inside the quarter's current fiber costs 2 LDS.128 + 4 LDG.128 (one
+// L1 wavefront per D row, the floor) + 8 FFMA2 with no masking; only a
+// quarter whose group crosses a fiber end takes the leaf-by-leaf path, and
+// that path closes the fiber (scale by the C row held in registers) without
+// touching the other quarters' leaves.  Fiber ends and k coordinates come from
+// an 8-fiber window held one per lane of the quarter (width-8 shuffles), the
+// next C row is loaded when a fiber opens and consumed when it closes.
+// ---------------------------------------------------------------------------
+#ifndef SPX_MTTKRP_QUARTER
+#define SPX_MTTKRP_QUARTER 1
+#endif
+#ifndef SPX_MQ_RING
+#define SPX_MQ_RING 2
+#endif
+#ifndef SPX_MQ_CARVEOUT
+#define SPX_MQ_CARVEOUT 14  // percent of 228 KB: the 32 KB shared-memory config, L1 keeps 224 KB for D
+#endif
+constexpr int kQRing = SPX_MQ_RING;       // slots of 8 leaves per quarter in flight
+#ifndef SPX_MQ_THREADS
+#define SPX_MQ_THREADS 512  // x 2 CTAs/SM (same-box A/B: 24 warps at 80 registers ran slower than 32 at 64)
+#endif
+#ifndef SPX_MQ_MINB
+#define SPX_MQ_MINB 2
+#endif
+constexpr int kQThreads = SPX_MQ_THREADS;
+constexpr int kQSlotBytes = 32 * 4 * 2;   // 32 crd + 32 vals (fp32)
+
+__device__ __forceinline__ int4 lds_i4(uint32_t a) {
+  int4 r;
+  asm volatile("ld.shared.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(a));
+  return r;
+}
+__device__ __forceinline__ float4 lds_f4(uint32_t a) {
+  float4 r;
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "r"(a));
+  return r;
+}
+__device__ __forceinline__ float4 ld_f4_na(const float4* p) {
+  float4 r;
+  asm("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ float4 ld_drow(const float4* p) {
+  // an explicit L2 policy (the descriptor becomes an immediate in a uniform
+  // register, so the loop needs no R2UR of the default descriptor per load)
+  return ld_f4_hint(p, kPolicyEvictLast);
+}
+__device__ __forceinline__ void red_add_f4(float* dst, float4 x) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(dst), "f"(x.x), "f"(x.y), "f"(x.z), "f"(x.w)
+               : "memory");
+}
+
+template <bool AL16>
+__global__ void __launch_bounds__(kQThreads, SPX_MQ_MINB) mttkrp_quarter_kernel(
+    const int32_t* __restrict__ crd0, const int32_t* __restrict__ pos1, const int32_t* __restrict__ crd1,
+    const int32_t* __restrict__ pos2, const int32_t* __restrict__ crd2, const float* __restrict__ vals,
+    const float* __restrict__ Cm, const float* __restrict__ Dm, float* __restrict__ A, int S, int F, int nnz,
+    int W, int nchunks, const int32_t* __restrict__ chunkF, const int32_t* __restrict__ chunkS, uint32_t rowb) {
+  // rowb = 128 (bytes per C / D row) arrives as a parameter so that row
+  // addresses stay one IMAD.WIDE.U32 (a literal 128 is strength-reduced to
+  // a three-instruction shift-and-add)
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qw = lane >> 3, ql = lane & 7;
+  const unsigned qmask = 0xFFu << (qw * 8);
+  unsigned char* ring = smem_raw + (size_t)warp * (kQRing * kQSlotBytes);
+  const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
+  const uint64_t pol_s = l2_evict_first();
+  // this lane's 16 B column slice of the C / D / A rows (row r at + r*128 B)
+  const char* __restrict__ Cl = reinterpret_cast<const char*>(Cm) + ql * 16;
+  const char* __restrict__ Dl = reinterpret_cast<const char*>(Dm) + ql * 16;
+  float* __restrict__ Al = A + ql * 4;
+  // the quarter's 8 leaf coordinates / values of a slot (broadcast LDS.128)
+  const int rd_off = qw * 32;
+  // AL16: lanes 0-3 of a quarter copy 16 B each -- (coordinates | values) x (leaves 0-3 | 4-7)
+  const int cp_h = ql & 1, cp_which = (ql >> 1) & 1;
+  const uint32_t cp_dst = (uint32_t)(cp_which * 128 + qw * 32 + cp_h * 16);
+  const char* cp_src = cp_which ? reinterpret_cast<const char*>(vals) : reinterpret_cast<const char*>(crd2);
+  const int Wq = W >> 2;
+  for (int q = blockIdx.x * nw + warp; q < nchunks; q += gridDim.x * nw) {
+    const int c0 = q * W, c1 = min(c0 + W, nnz);
+    const int a = min(c0 + qw * Wq, c1), b = min(a + Wq, c1);
+    const int nbw = (min(Wq, c1 - c0) + 7) >> 3;  // batches of 8 leaves (quarter 0 has the most)
+    // issue batch bi into ring slot `slot`
+    auto issue = [&](int bi, uint32_t slot) {
+      if (bi < nbw) {
+        if constexpr (AL16) {
+          if (ql < 4) {
+            const int p = a + bi * 8 + cp_h * 4;
+            const int nv = max(0, min(4, b - p));
+            cp_async16_zfill(ring_s + slot + cp_dst, cp_src + (size_t)(nv ? p : 0) * 4, nv * 4, pol_s);
+          }
+        } else {
+          const int p = a + bi * 8 + ql;
+          const bool ok = p < b;
+          cp_async4(ring_s + slot + lane * 4, crd2 + (ok ? p : 0), ok ? 4 : 0, pol_s);
+          cp_async4(ring_s + slot + 128 + lane * 4, vals + (ok ? p : 0), ok ? 4 : 0, pol_s);
+        }
+      }
+      cp_async_commit();
+    };
+    uint32_t rslot = 0, islot = (kQRing - 1) * kQSlotBytes;
+#pragma unroll
+    for (int bi = 0; bi < kQRing - 1; ++bi) issue(bi, bi * kQSlotBytes);
+    const bool live = a < b;
+    int f = live ? __ldg(chunkF + q * 4 + qw) : 0;
+    int s = live ? __ldg(chunkS + q * 4 + qw) : 0;
+    // fiber window: lane ql holds the end and k of fiber fb+ql
+    int fb = f;
+    int fe_w = ld_i32_first(pos2 + min(fb + 1 + ql, F), pol_s);
+    int k_w = ld_i32_first(crd1 + min(fb + ql, F - 1), pol_s);
+    int send = __ldg(pos1 + s + 1);
+    int fend = __shfl_sync(kFull, fe_w, 0, 8);
+    float4 crow = ld_f4_na(reinterpret_cast<const float4*>(addr_wide(Cl, (uint32_t)__shfl_sync(kFull, k_w, 0, 8), rowb)));
+    float2 af0 = make_float2(0.f, 0.f), af1 = af0, as0 = af0, as1 = af0;
+    // close fiber f (quarter-divergent: only this quarter's lanes run it)
+    auto close_fiber = [&]() {
+      as0 = __ffma2_rn(af0, make_float2(crow.x, crow.y), as0);
+      as1 = __ffma2_rn(af1, make_float2(crow.z, crow.w), as1);
+      af0 = make_float2(0.f, 0.f);
+      af1 = af0;
+      ++f;
+      if (f - fb >= 8) {
+        fb = f;
+        fe_w = ld_i32_first(pos2 + min(fb + 1 + ql, F), pol_s);
+        k_w = ld_i32_first(crd1 + min(fb + ql, F - 1), pol_s);
+      }
+      fend = __shfl_sync(qmask, fe_w, f - fb, 8);
+      while (f >= send) {
+        red_add_f4(Al + (int64_t)__ldg(crd0 + s) * 32, make_float4(as0.x, as0.y, as1.x, as1.y));
+        as0 = make_float2(0.f, 0.f);
+        as1 = as0;
+        ++s;
+        send = __ldg(pos1 + s + 1);
+      }
+      crow = ld_f4_na(reinterpret_cast<const float4*>(addr_wide(Cl, (uint32_t)__shfl_sync(qmask, k_w, f - fb, 8), rowb)));
+    };
+#define SPX_QF(vv, d)                                                            \
+  do {                                                                           \
+    af0 = __ffma2_rn(make_float2((vv), (vv)), make_float2((d).x, (d).y), af0); \
+    af1 = __ffma2_rn(make_float2((vv), (vv)), make_float2((d).z, (d).w), af1); \
+  } while (0)
+#define SPX_DR(l) ld_drow(reinterpret_cast<const float4*>(addr_wide(Dl, (uint32_t)(l), rowb)))
+    int pp = a;  // first leaf of the current group
+#pragma unroll 1
+    for (int bi = 0; bi < nbw; ++bi) {
+      issue(bi + kQRing - 1, islot);
+      islot = islot == (kQRing - 1) * kQSlotBytes ? 0 : islot + kQSlotBytes;
+      cp_async_wait<kQRing - 1>();
+      __syncwarp();
+      const uint32_t sl = ring_s + rslot + rd_off;
+      rslot = rslot == (kQRing - 1) * kQSlotBytes ? 0 : rslot + kQSlotBytes;
+#pragma unroll
+      for (int h = 0; h < 2; ++h, pp += 4) {
+        const int4 l4 = lds_i4(sl + h * 16);
+        const float4 d0 = SPX_DR(l4.x), d1 = SPX_DR(l4.y), d2 = SPX_DR(l4.z), d3 = SPX_DR(l4.w);
+        const float4 v4 = lds_f4(sl + 128 + h * 16);
+        if (pp + 4 <= fend) {  // leaves pp..pp+3 lie in fiber f (zero-filled past b)
+          SPX_QF(v4.x, d0);
+          SPX_QF(v4.y, d1);
+          SPX_QF(v4.z, d2);
+          SPX_QF(v4.w, d3);
+        } else if (pp < b) {
+          while (pp >= fend) close_fiber();
+          SPX_QF(v4.x, d0);
+          if (pp + 1 < b) {
+            while (pp + 1 >= fend) close_fiber();
+            SPX_QF(v4.y, d1);
+            if (pp + 2 < b) {
+              while (pp + 2 >= fend) close_fiber();
+              SPX_QF(v4.z, d2);
+              if (pp + 3 < b) {
+                while (pp + 3 >= fend) close_fiber();
+                SPX_QF(v4.w, d3);
+              }
+            }
+          }
+        }
+      }
+      __syncwarp();
+    }
+#undef SPX_QF
+#undef SPX_DR
+    // close the open fiber; fold the quarters when they end in one slice
+    as0 = __ffma2_rn(af0, make_float2(crow.x, crow.y), as0);
+    as1 = __ffma2_rn(af1, make_float2(crow.z, crow.w), as1);
+    float4 x = make_float4(as0.x, as0.y, as1.x, as1.y);
+    const int skey = live ? s : -1;
+    const bool same = __all_sync(kFull, __shfl_sync(kFull, skey, 0) == skey);
+    if (same) {
+#pragma unroll
+      for (int o = 8; o < 32; o <<= 1) {
+        x.x += __shfl_xor_sync(kFull, x.x, o);
+        x.y += __shfl_xor_sync(kFull, x.y, o);
+        x.z += __shfl_xor_sync(kFull, x.z, o);
+        x.w += __shfl_xor_sync(kFull, x.w, o);
+      }
+      if (qw == 0 && live) red_add_f4(Al + (int64_t)__ldg(crd0 + s) * 32, x);
+    } else if (live) {
+      red_add_f4(Al + (int64_t)__ldg(crd0 + s) * 32, x);
+    }
+  }
+  cp_async_wait<0>();
+}
+
+// the quarter kernel's shape: fp32, rank 32, NNZ_PER_WARP a multiple of 4,
+// 16 B aligned C / D / A rows (float4 loads, red.v4)
+bool mttkrp_quarter_ok(const Args& a) {
+  if (!SPX_MTTKRP_QUARTER || a.dtype != SPX_F32 || a.dims[1][1] != 32) return false;
+  const int64_t W = a.params[1];
+  if (W < 4 || W % 4 != 0) return false;
+  auto al = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
+  return (!a.vals[1] || al(a.vals[1])) && (!a.vals[2] || al(a.vals[2])) && (!a.out || al(a.out));
+}
+
 constexpr size_t kSmemBudget = 200 * 1024;
 
 // K8: persistent CTAs; warp-chunk q covers leaves [q*W, (q+1)*W) (the
@@ -634,6 +855,11 @@ int run_ttv(const Args& a) {
   return check_cuda(cudaGetLastError(), "ttv_rbk_kernel");
 }
 
+template <typename T>
+__global__ void ttv_prep_kernel(const int32_t* __restrict__ pos1, const int32_t* __restrict__ pos2,
+                                int32_t* __restrict__ chunkF, int32_t* __restrict__ chunkS, T* __restrict__ A,
+                                int64_t nA, int S, int F, int CH);
+
 template <typename T, int VPL, bool CONTIG>
 int run_mttkrp(int kid, const Args& a) {
   const Csf c = csf_of(a);
@@ -642,6 +868,47 @@ int run_mttkrp(int kid, const Args& a) {
   const T* vals = static_cast<const T*>(a.vals[0]);
   const T* Cm = static_cast<const T*>(a.vals[1]);
   const T* Dm = static_cast<const T*>(a.vals[2]);
+  if constexpr (std::is_same<T, float>::value && VPL == 1 && CONTIG && SPX_MTTKRP_QUARTER) {
+    if (kid == SPX_K_MTTKRP_NNZ && R == 32 && c.nnz > 0 && mttkrp_quarter_ok(a)) {
+      const int64_t TB = a.params[0], W = a.params[1];
+      if (TB < 1 || W < 1 || TB % W != 0 || TB / W > kMaxWarps)
+        return fail(SPX_E_UNSUPPORTED, "MTTKRP nnz-split needs NNZ_PER_TB a multiple of NNZ_PER_WARP, <= 16 warps");
+      const int64_t Wq = W / 4, nq = ceil_div(c.nnz, Wq), nchunks = ceil_div(c.nnz, W);
+      const size_t need = (size_t)2 * nq * sizeof(int32_t);
+      if (!a.ws || a.ws_bytes < need) return fail(SPX_E_WORKSPACE, "workspace %zu < %zu bytes", a.ws_bytes, need);
+      int32_t* chunkF = static_cast<int32_t*>(a.ws);
+      int32_t* chunkS = chunkF + nq;
+      const int64_t nA = I * R;
+      const int64_t prep_work =
+          std::max<int64_t>(std::max<int64_t>(ceil_div(c.F, 8), nA * (int64_t)sizeof(T) / 16), c.S * 32);
+      const int64_t prep_grid = std::min<int64_t>(ceil_div(prep_work, 256), (int64_t)num_sms() * 8);
+      // zero A and build the quarter-chunk table (fiber, slice holding each quarter chunk's first leaf)
+      ttv_prep_kernel<float><<<(unsigned)prep_grid, 256, 0, a.stream>>>(c.pos1, c.pos2, chunkF, chunkS, A, nA,
+                                                                         (int)c.S, (int)c.F, (int)Wq);
+      count_launch();
+      if (int e = check_cuda(cudaGetLastError(), "ttv_prep_kernel")) return e;
+      const size_t smem = (size_t)(kQThreads / 32) * kQRing * kQSlotBytes;
+      // 16 B leaf copies need every quarter chunk to start on a 4-leaf boundary
+      auto kern = W % 16 == 0 ? mttkrp_quarter_kernel<true> : mttkrp_quarter_kernel<false>;
+      static bool carve = [] {
+        cudaFuncSetAttribute(mttkrp_quarter_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             SPX_MQ_CARVEOUT);
+        cudaFuncSetAttribute(mttkrp_quarter_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             SPX_MQ_CARVEOUT);
+        return true;
+      }();
+      (void)carve;
+      int per_sm = 1;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kQThreads, smem);
+      if (per_sm < 1) per_sm = 1;
+      const int64_t grid = std::min<int64_t>((int64_t)num_sms() * per_sm, ceil_div(nchunks, kQThreads / 32));
+      kern<<<(unsigned)grid, kQThreads, smem, a.stream>>>(
+          c.crd0, c.pos1, c.crd1, c.pos2, c.crd2, vals, Cm, Dm, A, (int)c.S, (int)c.F, (int)c.nnz, (int)W,
+          (int)nchunks, chunkF, chunkS, (uint32_t)(R * sizeof(float)));
+      count_launch();
+      return check_cuda(cudaGetLastError(), "mttkrp_quarter_kernel");
+    }
+  }
   if (int e = check_cuda(cudaMemsetAsync(A, 0, (size_t)(I * R) * sizeof(T), a.stream), "memset")) return e;
   if (c.nnz == 0) return SPX_OK;
   const int nw = kMttkrpThreads / 32;
@@ -1064,7 +1331,9 @@ size_t ws_csf(int kid, const Args& a) {
   if (kid != SPX_K_MTTKRP_NNZ) return 0;
   const int64_t nnz = a.level_sizes[2];
   const int64_t W = a.params[1] > 0 ? a.params[1] : 1;
-  return (size_t)(ceil_div(nnz, W) + 1) * sizeof(int32_t);
+  size_t ws = (size_t)(ceil_div(nnz, W) + 1) * sizeof(int32_t);
+  if (mttkrp_quarter_ok(a)) ws = std::max(ws, (size_t)2 * (size_t)ceil_div(nnz > 0 ? nnz : 1, W / 4) * sizeof(int32_t));
+  return ws;
 }
 
 int launch_csf(int kid, const Args& a) {

@@ -238,7 +238,12 @@ def interpret(program: Program, inputs: dict, out_dims=None, *, dtype: str | Non
         dev_out = out if (out is not None and out.device.type == "cuda") else torch.empty(
             max(1, math.prod(odims)), dtype=torch_dtype(dtype), device=device)
         work = generic.launch(program, ops, dev_out, dtype, _cur_stream(device))
-        stats = generic.GenericStats(program, work)
+
+        def recount(program=program, ops=ops, n=dev_out.numel()):
+            scratch = torch.empty(n, dtype=torch_dtype(dtype), device=device)
+            return generic.launch(program, ops, scratch, dtype, _cur_stream(device), count=True)
+
+        stats = generic.GenericStats(program, work, recount if program.schedule_honoured else None)
         if out is not None:
             if out.device.type != "cuda":
                 out.copy_(dev_out.view_as(out), non_blocking=True)

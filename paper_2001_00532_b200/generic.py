@@ -1,31 +1,27 @@
-"""Generic lowering fallback: statements that no
-entry of the kernel-selection table matches run on the GPU through CUDA
-generated here and compiled at run time with NVRTC (`spx_jit_*`).
+"""Generic lowering: statements that no entry of the
+kernel-selection table matches run on the GPU through CUDA generated here and
+compiled at run time with NVRTC (`spx_jit_*`, csrc/spx_jit.cu).
 
-The generated code implements the statement's semantics, `dense_eval`
-(tensors.py:300-330) restricted to stored entries, for any right-hand side
-that expands to a sum of products of accesses and scalars (additive terms
-are evaluated one after the other into the same dense output, as dense_eval
-sums its einsum terms):
+The schedule is honoured: `irlower.lower_ir` lowers the scheduled statement
+into the reference's ImperativeIR -- the schedule's loop
+order, split/divide tails, pos/fuse position loops, coordinate recovery
+(SearchSegment / Track / SearchCoord), MaxExact asserts, parallel and unroll
+tags -- and `cuda_ir.emit` prints that IR as one CUDA kernel whose parallel
+loops are mapped onto blocks / warps / lanes as tagged.
+
+Statements `lower_ir` cannot express (pos over several accesses, ...) fall
+back to the unscheduled form below, flagged `schedule_honoured = False`
+with a warning: `dense_eval` (tensors.py:300-330) restricted to stored
+entries, for right-hand sides that expand to sums of products --
 
 * a term with a sparse operand is driven by the stored leaves of its first
-  sparse access -- one GPU thread per leaf (grid-stride), the leaf's
-  coordinates recovered level by level (`SearchSegment` over each compressed
-  level's pos, ir.py:178-190; div/mod for dense levels);
-* every other sparse access of the term is *located* at those coordinates
-  (`SearchCoord` over its crd, ir.py:193-205; a missing coordinate
-  contributes zero, which is the intersection merge of graph.py:92-100);
-* dense accesses are indexed row-major; variables the driver does not bind
-  are looped over their extents inside the thread;
-* a term without sparse operands is one thread per point of its iteration
-  space;
+  sparse access, one GPU thread per leaf, coordinates recovered level by
+  level (`SearchSegment`, ir.py:178-190);
+* other sparse accesses are located (`SearchCoord`, ir.py:193-205);
+* dense accesses are indexed row-major; other variables are looped inside;
 * contributions are added to the zeroed output with atomicAdd.
 
-This is the correctness path for schedules outside the table: the
-schedule's transformations do not change what a statement computes
-(SPEC.md §5), and this mapping ignores them -- the table's hand-tuned
-kernels are what honour them.  It is still GPU code end to end; there is
-no CPU fallback.
+There is no CPU fallback on either path.
 """
 
 from __future__ import annotations
@@ -99,6 +95,23 @@ class GenericProgram:
     params: list = field(default_factory=list)
     kernel: str = "generic_jit"
     kind: str = "generic"
+    ir_program: Any = None  # the schedule's ImperativeIR (None: unscheduled fallback)
+    loop_of: dict = field(default_factory=dict)  # IR loop variable -> forest variable
+    ir_error: str = ""
+
+    @property
+    def schedule_honoured(self) -> bool:
+        return self.ir_program is not None
+
+    def ir(self, dims: dict | None = None):
+        """The reference `ir.Program` (format_program / --dump-ir)."""
+        if self.ir_program is None:
+            raise _spindle.errors.LoweringError(f"no ImperativeIR for this statement: {self.ir_error}")
+        if dims is None:
+            return self.ir_program
+        from .irlower import lower_ir
+
+        return lower_ir(self.stmt, dims)
 
     @property
     def tensor_order(self) -> tuple:
@@ -112,7 +125,28 @@ class GenericProgram:
         return tuple(ext[v.name] for v in self.stmt.assignment.lhs.vars)
 
     def describe(self) -> str:
-        return f"generic:{self.kernel}"
+        return f"generic:{self.kernel}" + ("" if self.schedule_honoured else " (unscheduled)")
+
+
+def make_program(stmt, why: str = "", dims: dict | None = None) -> GenericProgram:
+    """Lower `stmt` to ImperativeIR; statements the IR lowering rejects get the
+    unscheduled term kernels, with a warning (the schedule is not honoured)."""
+    import warnings
+
+    from .irlower import lower_ir
+
+    E = _spindle.errors
+    try:
+        prog, loop_of = lower_ir(stmt, dims, meta=True)
+        return GenericProgram(stmt, why=why, dims=dims, ir_program=prog, loop_of=loop_of, kernel="generic_ir")
+    except E.LoweringError as err:
+        warnings.warn(f"schedule not honoured (unscheduled generic kernels): {err}", LoweringFallbackWarning,
+                      stacklevel=3)
+        return GenericProgram(stmt, why=why, dims=dims, ir_error=str(err))
+
+
+class LoweringFallbackWarning(UserWarning):
+    """A statement runs on a path that does not follow its schedule."""
 
 
 def check_supported(stmt) -> None:
@@ -363,8 +397,11 @@ def check_bounds(prog: "GenericProgram", ops: dict) -> None:
                     f"extent of {rel.source} is {e}")
 
 
-def launch(prog: GenericProgram, ops: dict, out: torch.Tensor, dtype: str, stream: int) -> dict:
-    """Zero `out` and run every term kernel; returns work counts."""
+def launch(prog: GenericProgram, ops: dict, out: torch.Tensor, dtype: str, stream: int, *,
+           count: bool = False) -> dict:
+    """Zero `out` and run the program; returns work counts."""
+    if prog.ir_program is not None:
+        return launch_ir(prog, ops, out, dtype, stream, count=count)
     check_bounds(prog, ops)
     g = _Gen(prog.stmt, {t: ops[t].dims for t in prog.tensor_order}, dtype)
     src, terms = g.source()
@@ -403,16 +440,205 @@ def launch(prog: GenericProgram, ops: dict, out: torch.Tensor, dtype: str, strea
     return work
 
 
-class GenericStats:
-    """ExecStats for the generic path: work per additive term (stored leaves
-    of the driving operand, or points of the iteration space)."""
+# ---------------------------------------------------------------------------
+# the IR path
+# ---------------------------------------------------------------------------
 
-    def __init__(self, prog: GenericProgram, work: dict):
+
+def _host_eval(e, dims_flat: list, manifest, ops: dict, order: list):
+    """Value of an IR expression on the host, or None when it depends on a
+    loop variable (pos loads read single elements from the device)."""
+    IR = _spindle.ir
+    if isinstance(e, IR.IntLit):
+        return int(e.value)
+    if isinstance(e, IR.DimRef):
+        return int(dims_flat[manifest.dim_index(e.tensor, e.level)])
+    if isinstance(e, IR.BinOp):
+        a = _host_eval(e.lhs, dims_flat, manifest, ops, order)
+        b = _host_eval(e.rhs, dims_flat, manifest, ops, order)
+        if a is None or b is None:
+            return None
+        if e.op == "+":
+            return a + b
+        if e.op == "-":
+            return a - b
+        if e.op == "*":
+            return a * b
+        if e.op == "/":
+            return a // b if b else None
+        if e.op == "%":
+            return a % b if b else None
+        if e.op == "min":
+            return min(a, b)
+        return None
+    if isinstance(e, IR.Load) and e.array.kind == "pos":
+        i = _host_eval(e.index, dims_flat, manifest, ops, order)
+        if i is None:
+            return None
+        arr = ops[e.array.tensor].pos[e.array.level]
+        return int(arr[i].item())
+    return None
+
+
+def _launch_shape(prog, em, dims_flat, ops) -> tuple[int, int]:
+    from . import cuda_ir
+
+    ir_prog = prog.ir_program
+    order = [s.name for s in ir_prog.manifest.tensors]
+    ext = {}
+    for var, unit, lo, hi in cuda_ir.parallel_loops(ir_prog):
+        a = _host_eval(lo, dims_flat, ir_prog.manifest, ops, order)
+        b = _host_eval(hi, dims_flat, ir_prog.manifest, ops, order)
+        ext[unit] = None if a is None or b is None else max(0, b - a)
+    m = em.mapping
+    cap = 148 * 16
+    if "Global" in m:
+        n = ext.get("Global")
+        block = 256
+        grid = cap if n is None else max(1, min(cap, -(-n // block)))
+        return grid, block
+    if "GPUWarp" in m:
+        w = ext.get("GPUWarp")
+        block = 32 * (8 if w is None else max(1, min(32, w)))
+    elif "GPUThread" in m:
+        t = ext.get("GPUThread")
+        block = 256 if t is None else max(32, min(1024, -(-t // 32) * 32))
+    else:
+        block = 32
+    if "GPUBlock" in m:
+        b = ext.get("GPUBlock")
+        grid = 148 * 8 if b is None else max(1, min(cap, b))
+    else:
+        grid = 1
+    return grid, block
+
+
+def _atomic_needed(prog, em) -> bool:
+    """Plain += when every mapped loop writes disjoint outputs (NoRaces tag,
+    or the reference's structural test for an untagged spread loop)."""
+    S = _spindle.schedule
+    loops: list = []
+    em._walk(prog.ir_program.body, loops)
+    for lp in loops:
+        if lp.var not in em.by_var:
+            continue
+        if lp.parallel is not None:
+            if lp.parallel[1] != "NoRaces":
+                return True
+            continue
+        fv = prog.loop_of.get(lp.var, lp.var)
+        try:
+            if not S._writes_disjoint(prog.stmt, fv):
+                return True
+        except Exception:  # noqa: BLE001 - be conservative
+            return True
+    return False
+
+
+def launch_ir(prog: GenericProgram, ops: dict, out: torch.Tensor, dtype: str, stream: int, *,
+              count: bool = False) -> dict:
+    from . import cuda_ir
+
+    E = _spindle.errors
+    ir_prog = prog.ir_program
+    order = [s.name for s in ir_prog.manifest.tensors]
+    dims_flat = [int(d) for t in order for d in ops[t].dims]
+    em0 = cuda_ir._Emit(ir_prog, dtype, True, False)
+    atomic = _atomic_needed(prog, em0)
+    grid, block = _launch_shape(prog, em0, dims_flat, ops)
+    inst_plan = {}
+    n_inst = 0
+    if count:
+        for var, unit, lo, hi in cuda_ir.parallel_loops(ir_prog):
+            a = _host_eval(lo, dims_flat, ir_prog.manifest, ops, order)
+            b = _host_eval(hi, dims_flat, ir_prog.manifest, ops, order)
+            if a is not None and b is not None and 0 <= b - a <= (1 << 24):
+                inst_plan[var] = (n_inst, b - a)
+                n_inst += b - a
+    em = cuda_ir.emit(ir_prog, dtype, atomic=atomic, count=count, inst_plan=inst_plan)
+    fn = _function(em.src, cuda_ir.KERNEL)
+    dev = out.device
+    out.zero_()
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    cnt = torch.zeros(max(1, len(em.loops)), dtype=torch.int64, device=dev)
+    gcnt = torch.zeros(max(1, len(em.guard_tags)), dtype=torch.int64, device=dev)
+    bcnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    icnt = torch.zeros(max(1, n_inst), dtype=torch.int64, device=dev)
+    vals: list = [ctypes.c_void_p(out.data_ptr())]
+    for t, slot in zip(order, ir_prog.manifest.tensors):
+        d = ops[t]
+        vals.append(ctypes.c_void_p(d.vals.data_ptr()))
+        for lvl, ch in enumerate(slot.shorthand):
+            if ch == "s":
+                vals.append(ctypes.c_void_p(d.pos[lvl].data_ptr()))
+                vals.append(ctypes.c_void_p(d.crd[lvl].data_ptr()))
+    nd = max(1, len(dims_flat))
+    dims_arr = (ctypes.c_longlong * nd)(*(dims_flat or [0]))
+    vals.append(dims_arr)
+    for t_ in (err, cnt, gcnt, bcnt, icnt):
+        vals.append(ctypes.c_void_p(t_.data_ptr()))
+    ptrs = (ctypes.c_void_p * len(vals))(*[ctypes.cast(ctypes.pointer(v), ctypes.c_void_p) if not isinstance(
+        v, ctypes.Array) else ctypes.cast(v, ctypes.c_void_p) for v in vals])
+    lib = _lib.load()
+    _lib.check(lib.spx_jit_launch(ctypes.c_void_p(fn), grid, block, ptrs, ctypes.c_void_p(stream)),
+               "spx_jit_launch")
+    if int(err.item()) != 0:
+        raise E.ContractViolation("MaxExact bound violated: a bound(..., MaxExact) extent differs at run time")
+    work = {"grid": grid, "block": block, "atomic": atomic}
+    if count:
+        c = cnt.cpu().numpy()
+        loops: dict = {}
+        for k, v in enumerate(em.loops):
+            fv = prog.loop_of.get(v, v)
+            loops[fv] = loops.get(fv, 0) + int(c[k])
+        g = gcnt.cpu().numpy()
+        guards: dict = {}
+        for k, tag in enumerate(em.guard_tags):
+            guards[tag] = guards.get(tag, 0) + int(g[k])
+        ic = icnt.cpu().numpy()
+        inst = {prog.loop_of.get(v, v): ic[o:o + n].astype(np.int64) for v, (o, n) in inst_plan.items()}
+        work.update(loops=loops, guards=guards, body=int(bcnt.item()), instances=inst)
+    return work
+
+
+class GenericStats:
+    """ExecStats for the generic path.  On the IR path the
+    per-loop iteration counts, guard failures and per-parallel-instance work
+    are counted on the device by a counting launch of the same kernel into a
+    scratch output, run the first time a count is read; the unscheduled
+    fallback reports work per term."""
+
+    def __init__(self, prog: GenericProgram, work: dict, recount=None):
         self.program = prog
         self.kernel = prog.kernel
-        self.instance_work = {}
-        self.loop_counts = dict(work)
-        self.guard_failures = {}
+        self._work = dict(work)
+        self._recount = recount
+
+    def _counted(self) -> dict:
+        if "loops" not in self._work and self._recount is not None:
+            self._work.update(self._recount())
+            self._recount = None
+        return self._work
+
+    @property
+    def instance_work(self) -> dict:
+        return dict(self._counted().get("instances", {}))
+
+    @property
+    def loop_counts(self) -> dict:
+        w = self._counted()
+        return dict(w.get("loops", {k: v for k, v in w.items() if k.startswith("term")}))
+
+    @property
+    def guard_failures(self) -> dict:
+        return dict(self._counted().get("guards", {}))
+
+    @property
+    def body_visits(self):
+        return self._counted().get("body")
+
+    def work(self, var: str):
+        return self.instance_work[var]
 
     def summary(self) -> dict:
-        return {"kernel": self.kernel, "terms": self.loop_counts}
+        return {"kernel": self.kernel, "loops": self.loop_counts, "guards": self.guard_failures}

@@ -229,6 +229,14 @@ class Program:
                       for t in self.tensor_order)
         return IR.Manifest(tensors=slots, out_dims=self.out_dims(dims))
 
+    def ir(self, dims: dict | None = None):
+        """The statement's ImperativeIR as the reference `ir.Program`
+        (ir.py:267-273), the same lowering the generic path runs
+        (irlower.lower_ir): `format_program` / --dump-ir consume it."""
+        from .irlower import lower_ir
+
+        return lower_ir(self.stmt, dims if dims is not None else self.dims)
+
     def out_dims(self, dims: dict) -> tuple:
         ext = {}
         for acc in self.stmt.assignment.input_accesses():
@@ -577,10 +585,10 @@ def lower(stmt, formats=None, dims=None, *, fallback: bool = True):
     except E.LoweringError as err:
         if not fallback or "disagrees with the concretized statement" in str(err):
             raise
-        from .generic import GenericProgram, check_supported
+        from .generic import check_supported, make_program
 
         check_supported(stmt)
-        return GenericProgram(stmt, why=str(err), dims=dict(dims) if dims is not None else None)
+        return make_program(stmt, why=str(err), dims=dict(dims) if dims is not None else None)
 
 
 def _lower_table(stmt, formats=None, dims=None) -> Program:

@@ -58,7 +58,8 @@ def time_launch(ex: Executor, flush: torch.Tensor, reps: int, warm: int) -> list
 
 def pick(schedules, args):
     only = [x for x in args.only.split(",") if x]
-    return [s for s in schedules if not only or s[0] in only]
+    extra = {k: int(v) for k, v in (kv.split("=") for kv in args.params.split(",") if kv)}
+    return [(s[0], {**s[1], **extra}) for s in schedules if not only or s[0] in only]
 
 
 def rel_err(got: np.ndarray, want: np.ndarray) -> float:
@@ -180,6 +181,7 @@ def main():
     ap.add_argument("--warm", type=int, default=8)
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--only", default="", help="comma list of schedule names to run (default all)")
+    ap.add_argument("--params", default="", help="K=V,... schedule constants merged into the picked schedules")
     args = ap.parse_args()
     PEAK = hbm_peak()
     FLUSH = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
