@@ -226,11 +226,14 @@ int spx_selftest(uint64_t* out4, void* stream);
  * 1 = FROSTT.  spx_text_scan reports order, entry count and dims (FROSTT:
  * the last '# dims:' comment, or -1 = infer); spx_text_parse writes 0-based
  * int32 coordinates (level-major, coords[l*n + i]) and fp64 values in file
- * order into HOST buffers and fills inferred FROSTT dims.  Both return
- * SPX_PARSE_DEFER for any file they do not accept verbatim (malformed or
- * out-of-bounds entries, count mismatches, non-ASCII, Python-only literal
- * syntax); the host then runs the reference parser, which raises the exact
- * error (or accepts the literal).
+ * order into HOST buffers and fills inferred FROSTT dims.  Malformed files
+ * return SPX_PARSE_ERROR; spx_text_error then gives the reference's error
+ * class (1 TensorFileError, 2 HeaderError, 3 EntryBoundsError,
+ * 4 EntryValueError, errors.py:28-45), 1-based line and message -- the
+ * first error in file order, as fileio.py:66-162 raises it.  Only
+ * non-ASCII text, integers past 18 digits, orders outside 1..8 and
+ * dimensions past int32 return SPX_PARSE_DEFER (the host runs the
+ * reference parser).
  */
 /*
  * Runtime compilation for the generic lowering fallback (generic.py): NVRTC
@@ -246,10 +249,12 @@ int spx_jit_launch(void* fn, uint32_t grid, uint32_t block, void** args,
 const char* spx_jit_log(void);
 
 #define SPX_PARSE_DEFER 1
+#define SPX_PARSE_ERROR 2
 int spx_text_scan(const char* text, int64_t len, int32_t fmt, int32_t* order_out,
                   int64_t* n_out, int64_t* dims_out);
 int spx_text_parse(const char* text, int64_t len, int32_t fmt, int32_t order,
                    int64_t n, int64_t* dims, int32_t* coords, double* vals);
+int spx_text_error(int32_t* kind, int64_t* line, char* msg, int64_t cap);
 
 size_t spx_pack_workspace_size(int64_t n, int32_t order);
 int spx_pack_sort(const int32_t* const* coords_host, int32_t order,
@@ -274,6 +279,38 @@ int spx_pack_level_fill(const int32_t* ucoord, int64_t nu,
                         int32_t* pos_out, int64_t* cpar, void* stream);
 int spx_pack_vals(const int64_t* slot, const double* uvals, int64_t nu,
                   void* vals_out, int32_t dtype, void* stream);
+
+/*
+ * Device-resident COO / hierarchy checks and conversions (formats.DeviceCoo,
+ * formats.DeviceTensor), csrc/spx_coo.cu.  Orders 1..8; every array DEVICE
+ * unless marked host.
+ * spx_coo_check: *first_bad = first input index i (input order) whose
+ *   coordinate lies outside [0, dims) -- CooTensor.validate's bounds check
+ *   (tensors.py:75-81) -- or UINT64_MAX.  coords_host/dims as spx_pack_sort_strided.
+ * spx_unpack: coords_out[l*nleaves + q] = level-l coordinate of stored leaf
+ *   slot q, storage order -- Tensor.walk_stored (tensors.py:190-206).
+ *   levels = host "ds.." string, pos_host/crd_host = host tables of device
+ *   pointers (NULL for dense levels), level_sizes = host int64[order].
+ * spx_check_invariants: one compressed level of Tensor.check_invariants
+ *   (tensors.py:147-163): *result = min over violations of
+ *   (level << 40) | (code << 36) | segment, code 1 malformed pos, 2 pos not
+ *   nondecreasing, 3 segment not strictly increasing; UINT64_MAX if none.
+ * spx_scatter_dense: out[row-major linearised coords[i]] = vals[i]
+ *   (Tensor.to_dense, tensors.py:181-188); dtype SPX_F64 / SPX_F32.
+ */
+int spx_coo_check(const int32_t* const* coords_host, int64_t coord_stride,
+                  int32_t order, const int64_t* dims, int64_t n,
+                  uint64_t* first_bad, void* stream);
+int spx_unpack(int32_t order, const char* levels, const int64_t* dims,
+               const int32_t* const* pos_host, const int32_t* const* crd_host,
+               const int64_t* level_sizes, int64_t nleaves, int32_t* coords_out,
+               void* stream);
+int spx_check_invariants(const int32_t* pos, const int32_t* crd, int64_t count,
+                         int64_t ncrd, int32_t level, uint64_t* result,
+                         void* stream);
+int spx_scatter_dense(const int32_t* const* coords_host, int64_t coord_stride,
+                      int32_t order, const int64_t* dims, int64_t n,
+                      const void* vals, int32_t dtype, void* out, void* stream);
 
 #ifdef __cplusplus
 }

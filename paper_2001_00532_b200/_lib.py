@@ -71,8 +71,13 @@ EXPORTS = (
     "spx_pack_level",
     "spx_pack_level_fill",
     "spx_pack_vals",
+    "spx_coo_check",
+    "spx_unpack",
+    "spx_check_invariants",
+    "spx_scatter_dense",
     "spx_text_scan",
     "spx_text_parse",
+    "spx_text_error",
     "spx_jit_compile",
     "spx_jit_launch",
     "spx_jit_log",
@@ -158,10 +163,21 @@ def load(path: str | os.PathLike | None = None):
     lib.spx_pack_level_fill.restype = ctypes.c_int
     lib.spx_pack_vals.argtypes = [vp, vp, i64, vp, ctypes.c_int32, vp]
     lib.spx_pack_vals.restype = ctypes.c_int
+    lib.spx_coo_check.argtypes = [ctypes.POINTER(vp), i64, ctypes.c_int32, i64p, i64, vp, vp]
+    lib.spx_coo_check.restype = ctypes.c_int
+    lib.spx_unpack.argtypes = [ctypes.c_int32, ctypes.c_char_p, i64p, ctypes.POINTER(vp), ctypes.POINTER(vp), i64p,
+                               i64, vp, vp]
+    lib.spx_unpack.restype = ctypes.c_int
+    lib.spx_check_invariants.argtypes = [vp, vp, i64, i64, ctypes.c_int32, vp, vp]
+    lib.spx_check_invariants.restype = ctypes.c_int
+    lib.spx_scatter_dense.argtypes = [ctypes.POINTER(vp), i64, ctypes.c_int32, i64p, i64, vp, ctypes.c_int32, vp, vp]
+    lib.spx_scatter_dense.restype = ctypes.c_int
     lib.spx_text_scan.argtypes = [ctypes.c_char_p, i64, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32), i64p, i64p]
     lib.spx_text_scan.restype = ctypes.c_int
     lib.spx_text_parse.argtypes = [ctypes.c_char_p, i64, ctypes.c_int32, ctypes.c_int32, i64, i64p, vp, vp]
     lib.spx_text_parse.restype = ctypes.c_int
+    lib.spx_text_error.argtypes = [ctypes.POINTER(ctypes.c_int32), i64p, ctypes.c_char_p, i64]
+    lib.spx_text_error.restype = ctypes.c_int
     lib.spx_jit_compile.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, ctypes.POINTER(vp)]
     lib.spx_jit_compile.restype = ctypes.c_int
     lib.spx_jit_launch.argtypes = [vp, ctypes.c_uint32, ctypes.c_uint32, ctypes.POINTER(vp), vp]

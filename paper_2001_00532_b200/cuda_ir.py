@@ -96,26 +96,41 @@ class _Emit:
         elif isinstance(s, IR.WhileLoop):
             self._walk(s.body, out)
 
+    def _roots(self) -> list:
+        """Top-level nests: one per additive term (lower_ir wraps each term of
+        a multi-term statement in its own Block)."""
+        IR = _ir()
+        st = self.p.body.stmts
+        if len(st) > 1 and all(isinstance(x, IR.Block) for x in st):
+            return list(st)
+        return [self.p.body]
+
     def _plan_units(self):
-        loops: list = []
-        self._walk(self.p.body, loops)
+        """Map parallel units per term nest: the first loop carrying each GPU
+        unit; without GPU units the first CPUThread loop, else the outermost
+        loop, spreads over all threads ("Global")."""
         gpu = {"GPUBlock", "GPUWarp", "GPUThread"}
-        for lp in loops:
-            if lp.parallel is None:
-                continue
-            unit = lp.parallel[0]
-            if unit in self.mapping.values():
-                continue
-            if unit in gpu and unit not in self.mapping:
-                self.mapping[unit] = lp.var
-        if not (gpu & set(self.mapping)):
+        self.by_var: dict = {}
+        self.term_units: list = []
+        self.mapping: dict = {}
+        for root in self._roots():
+            loops: list = []
+            self._walk(root, loops)
+            units: dict = {}
             for lp in loops:
-                if lp.parallel is not None and lp.parallel[0] == "CPUThread":
-                    self.mapping["Global"] = lp.var
-                    break
-        if not self.mapping and loops:
-            self.mapping["Global"] = loops[0].var  # unscheduled: spread the outermost loop
-        self.by_var = {v: u for u, v in self.mapping.items()}
+                if lp.parallel is not None and lp.parallel[0] in gpu and lp.parallel[0] not in units:
+                    units[lp.parallel[0]] = lp.var
+            if not units:
+                cpu = next((lp for lp in loops if lp.parallel is not None and lp.parallel[0] == "CPUThread"), None)
+                if cpu is not None:
+                    units["Global"] = cpu.var
+                elif loops:
+                    units["Global"] = loops[0].var  # unscheduled: spread the outermost loop
+            self.term_units.append(units)
+            for u, v in units.items():
+                self.by_var[v] = u
+                self.mapping.setdefault(u, v)
+        self.cur_units = self.term_units[0] if self.term_units else {}
 
     def index_of(self, unit: str) -> tuple[str, str]:
         if unit == "GPUBlock":
@@ -123,21 +138,22 @@ class _Emit:
         if unit == "GPUWarp":
             return "(ll)(threadIdx.x >> 5)", "(ll)(blockDim.x >> 5)"
         if unit == "GPUThread":
-            if "GPUWarp" in self.mapping:
+            if "GPUWarp" in self.cur_units:
                 return "(ll)(threadIdx.x & 31)", "32LL"
             return "(ll)threadIdx.x", "(ll)blockDim.x"
         return "((ll)blockIdx.x * blockDim.x + threadIdx.x)", "((ll)gridDim.x * blockDim.x)"
 
-    def active(self) -> str:
+    def active(self, units: dict) -> str:
+        """Hardware threads a term nest runs on: lanes / warps / blocks no
+        loop of the nest maps would repeat its work, so they sit it out."""
+        if "Global" in units or not units:
+            return "" if units else "blockIdx.x == 0 && threadIdx.x == 0"
         conds = []
-        m = self.mapping
-        if "Global" in m:
-            return ""
-        if "GPUThread" not in m:
-            conds.append("(threadIdx.x & 31) == 0" if "GPUWarp" in m else "threadIdx.x == 0")
-        if "GPUWarp" not in m and "GPUThread" in m:
-            pass
-        if "GPUBlock" not in m:
+        if "GPUThread" not in units:
+            conds.append("(threadIdx.x & 31) == 0" if "GPUWarp" in units else "threadIdx.x == 0")
+        if "GPUWarp" not in units and "GPUThread" in units:
+            pass  # the thread loop strides over the whole block
+        if "GPUBlock" not in units:
             conds.append("blockIdx.x == 0")
         return " && ".join(conds)
 
@@ -247,7 +263,7 @@ class _Emit:
             out.append(f"{pad}ll v_{st.result} = spx_lb({self.arr(st.array)}, {self.e(st.lo)}, {self.e(st.hi)}, "
                        f"{self.e(st.key)});")
         elif isinstance(st, IR.AssertExtent):
-            out.append(f"{pad}if ({self.e(st.actual)} != {self.e(st.expected)}) {{ atomicExch(err, 1); return; }}")
+            out.append(f"{pad}if ({self.e(st.actual)} != {self.e(st.expected)}) {{ atomicExch(err, 1); return; }}")  # noqa
         elif isinstance(st, IR.AllocWorkspace):
             raise TypeError("workspaces are not emitted")
         else:
@@ -269,12 +285,14 @@ class _Emit:
         self.inst = dict(inst_plan or {})
         nd = max(1, sum(len(s.dims) for s in self.p.manifest.tensors))
         body: list = []
-        self.s(self.p.body, 1, body, [])
-        act = self.active()
+        for root, units in zip(self._roots(), self.term_units):
+            self.cur_units = units
+            act = self.active(units)
+            body.append(f"  if ({act or 'true'}) {{")
+            self.s(root, 2, body, [])
+            body.append("  }")
         lines = [_PRELUDE % {"T": self.T, "ND": nd},
                  f'extern "C" __global__ void __launch_bounds__(1024) {KERNEL}(' + ", ".join(self.params()) + ") {"]
-        if act:
-            lines.append(f"  if (!({act})) return;")
         lines += body
         lines.append("}")
         return Emitted("\n".join(lines) + "\n", self.loops, self.guard_tags, dict(self.mapping), self.inst)

@@ -4,12 +4,11 @@
 (fileio.py:38-49, tensors.py:212-258) for large files: the text is parsed
 by the native multithreaded reader in libspx.so (`spx_text_scan` /
 `spx_text_parse`) into coordinate arrays, and `pack.pack_device` builds the
-hierarchy on the GPU.  The native reader accepts exactly the files the
-reference accepts in their plain form; for anything else (a malformed or
-out-of-bounds entry, a count mismatch, non-ASCII text, Python-only literals
-such as `1_000` or `inf`) it defers, and the reference parser runs instead
--- raising its own error class, message and line number, or returning the
-entries it accepts -- so results and errors are the reference's.
+hierarchy on the GPU.  The native reader accepts what the reference accepts
+(int() / float() literal syntax included) and raises the reference's error
+class with its message and line number for every malformed file
+(`spx_text_error`).  Only non-ASCII text, integers past 18 digits, orders
+outside 1..8 and dimensions beyond int32 are handed to the reference parser.
 """
 
 from __future__ import annotations
@@ -34,20 +33,38 @@ def _format_of(path: Path, text: str) -> int:
     return MATRIX_MARKET if text.lstrip().lower().startswith("%%matrixmarket") else FROSTT
 
 
+PARSE_DEFER, PARSE_ERROR = 1, 2
+
+
+def _raise_native_error(lib):
+    E = _spindle.errors
+    kind = ctypes.c_int32(0)
+    line = ctypes.c_int64(0)
+    buf = ctypes.create_string_buffer(4096)
+    lib.spx_text_error(ctypes.byref(kind), ctypes.byref(line), buf, len(buf))
+    cls = {1: E.TensorFileError, 2: E.HeaderError, 3: E.EntryBoundsError, 4: E.EntryValueError}[int(kind.value)]
+    raise cls(buf.value.decode("ascii", errors="replace"), int(line.value))
+
+
 def parse_native(data: bytes, fmt: int):
     """(dims, coords[n, order] int32 0-based, values f64) in file order, or
-    None when the native reader defers to the reference parser."""
+    None when the native reader defers to the reference parser.  Malformed
+    files raise the reference's TensorFileError subclass."""
     lib = _lib.load()
     order = ctypes.c_int32(0)
     n = ctypes.c_int64(0)
     dims = (ctypes.c_int64 * 8)()
     st = lib.spx_text_scan(data, len(data), fmt, ctypes.byref(order), ctypes.byref(n), dims)
+    if st == PARSE_ERROR:
+        _raise_native_error(lib)
     if st != 0:
         return None
     k, m = int(order.value), int(n.value)
     coords = np.empty((k, max(m, 1)), dtype=np.int32)
     vals = np.empty(max(m, 1), dtype=np.float64)
     st = lib.spx_text_parse(data, len(data), fmt, k, m, dims, coords.ctypes.data, vals.ctypes.data)
+    if st == PARSE_ERROR:
+        _raise_native_error(lib)
     if st != 0:
         return None
     return tuple(int(dims[i]) for i in range(k)), coords[:, :m].T, vals[:m]

@@ -489,7 +489,11 @@ def _launch_shape(prog, em, dims_flat, ops) -> tuple[int, int]:
     for var, unit, lo, hi in cuda_ir.parallel_loops(ir_prog):
         a = _host_eval(lo, dims_flat, ir_prog.manifest, ops, order)
         b = _host_eval(hi, dims_flat, ir_prog.manifest, ops, order)
-        ext[unit] = None if a is None or b is None else max(0, b - a)
+        e = None if a is None or b is None else max(0, b - a)
+        if unit not in ext:
+            ext[unit] = e
+        elif ext[unit] is not None:
+            ext[unit] = None if e is None else max(ext[unit], e)
     m = em.mapping
     cap = 148 * 16
     if "Global" in m:

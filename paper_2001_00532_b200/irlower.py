@@ -282,11 +282,12 @@ class _TermLower:
         self.sym_of: dict[str, str] = {}
         self.loops: dict[str, tuple] = {}  # forest var -> (loop var, lo, hi)
         self.fmt = root.fmt
+        self._term_forest()
         self._choose_driver()
         self._plan_levels()
         # loop-variable names in use (a sparse loop over a compressed level is
         # named var+tensor, leaving the variable's own name for its coordinate)
-        self.taken = {"out"} | {v for v in root.forest
+        self.taken = {"out"} | {v for v in self.forest
                                 if not (v in self.lvl_of and self.mode.get(self.lvl_of[v]) == ("iter", v)
                                         and self.Dfmt[self.lvl_of[v]] == "s")}
 
@@ -321,6 +322,39 @@ class _TermLower:
     def guard(self, cond, tag: str) -> None:
         self.add(_Item("guard", "", expr_refs(cond), cond=cond, tag=tag))
 
+    def origins(self, name: str) -> set:
+        """Original variables a provenance variable derives from."""
+        S = _S()
+        rel = self.prov.producing(name)
+        if rel is None:
+            return {name}
+        if isinstance(rel, (S.SplitRel, S.DivideRel)):
+            return self.origins(rel.parent)
+        if isinstance(rel, S.FuseRel):
+            return self.origins(rel.left) | self.origins(rel.right)
+        if isinstance(rel, (S.PosRel, S.BoundRel)):
+            return self.origins(rel.source)
+        if isinstance(rel, S.CoordRel):
+            return self.origins(rel.source)
+        return set()
+
+    def _term_forest(self):
+        """The forest loops this term runs: dense_eval sums each additive
+        term over its own variables only, so loops over variables the term
+        (and the output) does not use are dropped; a loop mixing used and
+        unused variables cannot be split per term."""
+        used = {v.name for a in self.accs for v in a.vars} | {v.name for v in self.stmt.assignment.lhs.vars}
+        self.used = used
+        self.forest = []
+        for v in self.r.forest:
+            o = self.origins(v)
+            if o <= used:
+                self.forest.append(v)
+            elif o & used:
+                raise _err().LoweringError(
+                    f"loop {v!r} mixes variables {sorted(o & used)} of an additive term with {sorted(o - used)} "
+                    "that the term does not use")
+
     # -- the driving access ---------------------------------------------------
     def _choose_driver(self):
         S = _S()
@@ -348,7 +382,7 @@ class _TermLower:
     def _plan_levels(self):
         S = _S()
         prov = self.prov
-        forest = set(self.r.forest)
+        forest = set(self.forest)
         self.mode: dict[int, tuple] = {}
         if self.D is None:
             return
@@ -471,7 +505,7 @@ class _TermLower:
                 v = self.coord_at(k)
                 memo[key] = v
                 return v
-        if name in self.r.forest:
+        if name in self.forest:
             v = _ref(self.loops_var(name))
             memo[key] = v
             return v
@@ -634,8 +668,8 @@ class _TermLower:
                 e = self.ext(rel.source)
                 self.add(_Item("assert", "", expr_refs(e), [IR.AssertExtent(
                     e, _lit(rel.bound), f"MaxExact bound({rel.source}, {rel.bounded}, {rel.bound})")]))
-        # make sure every forest variable's loop exists and is used (visit-exactly-once)
-        for v in self.r.forest:
+        # every forest loop of this term exists (visit-exactly-once)
+        for v in self.forest:
             self.r.loop_bounds(self, v)
         # driver
         if self.D is not None:
@@ -649,7 +683,8 @@ class _TermLower:
         for acc in self.others:
             prod = self.mul(prod, self.access_value(acc))
         for v in self.stmt.assignment.all_vars:
-            self.value(v.name)
+            if v.name in self.used:
+                self.value(v.name)
         # forest variables not used by any original (cannot happen for valid graphs)
         idx = None
         lhs = list(self.stmt.assignment.lhs.vars)
@@ -756,11 +791,11 @@ class _Lowerer:
         IR = _ir()
         S = _S()
         idx, prod = t.build()
-        race_tags = [self.stmt.tags_for(v) for v in self.forest]
-        par = [(v, tg) for v, tg in zip(self.forest, race_tags) if tg.parallel_unit is not None]
+        race_tags = [self.stmt.tags_for(v) for v in t.forest]
+        par = [(v, tg) for v, tg in zip(t.forest, race_tags) if tg.parallel_unit is not None]
         atomic_any = any(tg.race is S.RaceStrategy.ATOMICS for _, tg in par)
         body_stmt = IR.ReduceAdd(IR.ArrayRef("out"), idx, prod, atomic=atomic_any)
-        loops = [(v,) + tuple(self.loop_bounds(t, v)) for v in self.forest]
+        loops = [(v,) + tuple(self.loop_bounds(t, v)) for v in t.forest]
         for v, ln, _, _ in loops:
             self.loop_of[ln] = v
         items = list(t.items)

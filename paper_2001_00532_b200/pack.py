@@ -110,10 +110,11 @@ def pack_device(dims, levels, coords, values, *, device=None, dtype: str = "f64"
 
 
 def pack_coo_device(coo, levels, *, device=None, dtype: str = "f64") -> DeviceTensor:
-    """`pack` of a reference `CooTensor` (tensors.py:64-90) on the GPU."""
-    coo.validate()  # the reference's own arity/bounds checks, same messages and order
-    n = len(coo.entries)
-    order = len(coo.dims)
-    coords = np.array([cc for cc, _ in coo.entries], dtype=np.int64).reshape(n, order)
-    values = np.array([float(x) for _, x in coo.entries], dtype=np.float64)
-    return pack_device(coo.dims, levels, coords, values, device=device, dtype=dtype)
+    """`pack` of a reference `CooTensor` (tensors.py:64-90) on the GPU: the
+    entries go to a `DeviceCoo` (arity checked while flattening, bounds on
+    the device, the reference's messages for the first bad entry), which is
+    then packed."""
+    from .formats import DeviceCoo
+
+    d = DeviceCoo.from_reference(coo, device=device or "cuda")
+    return d.pack(levels, dtype=dtype)

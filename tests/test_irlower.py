@@ -31,7 +31,7 @@ def run_ir(stmt, ins, **kw):
     seq = []
     names = [v.name for v in stmt.assignment.all_vars]
     loops, guards, visits = ir_eval.run(prog, irtools.ir_tensors(ins), out,
-                                        visit=lambda env: seq.append(tuple(env[n] for n in names)),
+                                        visit=lambda env: seq.append(tuple(env.get(n) for n in names)),
                                         errors=_spindle.errors)
     return prog, out[: want.size].reshape(want.shape), want, loops, guards, visits, seq
 
@@ -92,9 +92,6 @@ def test_split_tail_guards():
 def test_divide_chunks():
     stmt, ins = _vec(10)
     stmt = S.divide(stmt, "i", "i0", "i1", 4)
-    chunks = []
-    names = {}
-
     prog = lower_ir(stmt, {"x": (10,)})
     out = np.zeros(10)
     per = {}
@@ -222,3 +219,30 @@ def test_maxexact_assert_raises():
     ins = irtools.inputs(e, np.random.default_rng(0))
     with pytest.raises(_spindle.errors.ContractViolation):
         run_ir(stmt, ins)
+
+
+# -- statements outside the kernel table (the generic path's cases) -------------------
+
+
+def test_generic_cases_match_dense_eval():
+    """Union adds, sparse x sparse, other formats / mode orders, scalar factors,
+    terms over different variables: IR lowering == dense_eval (fp64)."""
+    from test_gpu_generic import CASES, _rand_tensor
+
+    for expr, formats, order, sched in CASES:
+        rng = np.random.default_rng(len(expr))
+        asg = N.parse_assignment(expr)
+        stmt = S.concretize(asg, formats, order)
+        if sched:
+            stmt = S.apply_schedule(stmt, sched)
+        ext, ins = {}, {}
+        for acc in asg.input_accesses():
+            if acc.tensor in ins:
+                continue
+            dims = []
+            for v in acc.vars:
+                ext.setdefault(v.name, int(rng.integers(3, 9)))
+                dims.append(ext[v.name])
+            ins[acc.tensor], _ = _rand_tensor(tuple(dims), formats.get(acc.tensor, "d" * len(dims)), rng)
+        _, got, want, *_ = run_ir(stmt, ins)
+        assert np.max(np.abs(got - want) / np.maximum(1.0, np.abs(want))) <= 1e-12, expr
