@@ -562,6 +562,9 @@ constexpr int kQRing = SPX_MQ_RING;       // slots of 8 leaves per quarter in fl
 #define SPX_MQ_MINB 2
 #endif
 constexpr int kQThreads = SPX_MQ_THREADS;
+#ifndef SPX_MQ_SMWIN
+#define SPX_MQ_SMWIN 1  // fiber window in shared memory (else per-lane registers + width-8 shuffles)
+#endif
 constexpr int kQSlotBytes = 32 * 4 * 2;   // 32 crd + 32 vals (fp32)
 
 __device__ __forceinline__ int4 lds_i4(uint32_t a) {
@@ -605,6 +608,9 @@ __global__ void __launch_bounds__(kQThreads, SPX_MQ_MINB) mttkrp_quarter_kernel(
   unsigned char* ring = smem_raw + (size_t)warp * (kQRing * kQSlotBytes);
   const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
   const uint64_t pol_s = l2_evict_first();
+#if SPX_MQ_SMWIN
+  __shared__ int s_qwin[kQThreads / 32][4][16];
+#endif
   // this lane's 16 B column slice of the C / D / A rows (row r at + r*128 B)
   const char* __restrict__ Cl = reinterpret_cast<const char*>(Cm) + ql * 16;
   const char* __restrict__ Dl = reinterpret_cast<const char*>(Dm) + ql * 16;
@@ -621,14 +627,18 @@ __global__ void __launch_bounds__(kQThreads, SPX_MQ_MINB) mttkrp_quarter_kernel(
     const int a = min(c0 + qw * Wq, c1), b = min(a + Wq, c1);
     const int nbw = (min(Wq, c1 - c0) + 7) >> 3;  // batches of 8 leaves (quarter 0 has the most)
     // issue batch bi into ring slot `slot`
+    // AL16: this lane's next 16 B source and how many of its leaves remain
+    const char* isrc = cp_src + (size_t)(a + cp_h * 4) * 4;
+    int irem = b - (a + cp_h * 4);
     auto issue = [&](int bi, uint32_t slot) {
       if (bi < nbw) {
         if constexpr (AL16) {
           if (ql < 4) {
-            const int p = a + bi * 8 + cp_h * 4;
-            const int nv = max(0, min(4, b - p));
-            cp_async16_zfill(ring_s + slot + cp_dst, cp_src + (size_t)(nv ? p : 0) * 4, nv * 4, pol_s);
+            const int nv = max(0, min(4, irem));
+            cp_async16_zfill(ring_s + slot + cp_dst, nv ? isrc : cp_src, nv * 4, pol_s);
           }
+          isrc += 32;
+          irem -= 8;
         } else {
           const int p = a + bi * 8 + ql;
           const bool ok = p < b;
@@ -644,6 +654,47 @@ __global__ void __launch_bounds__(kQThreads, SPX_MQ_MINB) mttkrp_quarter_kernel(
     const bool live = a < b;
     int f = live ? __ldg(chunkF + q * 4 + qw) : 0;
     int s = live ? __ldg(chunkS + q * 4 + qw) : 0;
+#if SPX_MQ_SMWIN
+    // fiber window in shared memory: ends and k of fibers fb..fb+7 per
+    // quarter, read with broadcast LDS in the quarter-divergent close path
+    // (a shuffle there costs a warp-convergence check sequence)
+    int* const wend = s_qwin[threadIdx.x >> 5][qw];
+    int* const wk = wend + 8;
+    int fb = f;
+    wend[ql] = ld_i32_first(pos2 + min(fb + 1 + ql, F), pol_s);
+    wk[ql] = ld_i32_first(crd1 + min(fb + ql, F - 1), pol_s);
+    __syncwarp();
+    int send = __ldg(pos1 + s + 1);
+    int fend = wend[0];
+    float4 crow = ld_f4_na(reinterpret_cast<const float4*>(addr_wide(Cl, (uint32_t)wk[0], rowb)));
+    float2 af0 = make_float2(0.f, 0.f), af1 = af0, as0 = af0, as1 = af0;
+    // close fiber f (quarter-divergent: only this quarter's lanes run it)
+    auto close_fiber = [&]() {
+      as0 = __ffma2_rn(af0, make_float2(crow.x, crow.y), as0);
+      as1 = __ffma2_rn(af1, make_float2(crow.z, crow.w), as1);
+      af0 = make_float2(0.f, 0.f);
+      af1 = af0;
+      ++f;
+      if (f - fb >= 8) {
+        fb = f;
+        const int e_ = ld_i32_first(pos2 + min(fb + 1 + ql, F), pol_s);
+        const int k_ = ld_i32_first(crd1 + min(fb + ql, F - 1), pol_s);
+        __syncwarp(qmask);
+        wend[ql] = e_;
+        wk[ql] = k_;
+        __syncwarp(qmask);
+      }
+      fend = wend[f - fb];
+      while (f >= send) {
+        red_add_f4(Al + (int64_t)__ldg(crd0 + s) * 32, make_float4(as0.x, as0.y, as1.x, as1.y));
+        as0 = make_float2(0.f, 0.f);
+        as1 = as0;
+        ++s;
+        send = __ldg(pos1 + s + 1);
+      }
+      crow = ld_f4_na(reinterpret_cast<const float4*>(addr_wide(Cl, (uint32_t)wk[f - fb], rowb)));
+    };
+#else
     // fiber window: lane ql holds the end and k of fiber fb+ql
     int fb = f;
     int fe_w = ld_i32_first(pos2 + min(fb + 1 + ql, F), pol_s);
@@ -674,6 +725,7 @@ __global__ void __launch_bounds__(kQThreads, SPX_MQ_MINB) mttkrp_quarter_kernel(
       }
       crow = ld_f4_na(reinterpret_cast<const float4*>(addr_wide(Cl, (uint32_t)__shfl_sync(qmask, k_w, f - fb, 8), rowb)));
     };
+#endif
 #define SPX_QF(vv, d)                                                            \
   do {                                                                           \
     af0 = __ffma2_rn(make_float2((vv), (vv)), make_float2((d).x, (d).y), af0); \

@@ -222,7 +222,7 @@ class _Emit:
             else:
                 out.append(f"{pad}for (ll {v} = {lo}; {v} < {hi}; ++{v}) {{")
             if self.count:
-                out.append(f"{pad}  atomicAdd(cnt + {k}, 1ULL);")
+                out.append(f"{pad}  ++lc{k};")
             ctx = body_ctx + ([st] if st.parallel is not None or unit is not None else [])
             self.s(st.body, ind + 1, out, ctx)
             out.append(pad + "}")
@@ -238,7 +238,7 @@ class _Emit:
                 if self.count:
                     g = len(self.guard_tags)
                     self.guard_tags.append(st.tag)
-                    out.append(f"{pad}  atomicAdd(gcnt + {g}, 1ULL);")
+                    out.append(f"{pad}  ++lg{g};")
                 if st.orelse is not None:
                     self.s(st.orelse, ind + 1, out, body_ctx)
             out.append(pad + "}")
@@ -249,7 +249,7 @@ class _Emit:
             else:
                 out.append(f"{pad}{tgt} += (T)({self.e(st.value)});")
             if self.count:
-                out.append(f"{pad}atomicAdd(bcnt, 1ULL);")
+                out.append(f"{pad}++lb;")
                 for lp in body_ctx:
                     if lp.var in self.inst:
                         off = self.inst[lp.var][0]
@@ -293,7 +293,16 @@ class _Emit:
             body.append("  }")
         lines = [_PRELUDE % {"T": self.T, "ND": nd},
                  f'extern "C" __global__ void __launch_bounds__(1024) {KERNEL}(' + ", ".join(self.params()) + ") {"]
+        if self.count:
+            # per-thread counters (registers), one atomic each at the end
+            lines += [f"  unsigned long long lc{k} = 0;" for k in range(len(self.loops))]
+            lines += [f"  unsigned long long lg{g} = 0;" for g in range(len(self.guard_tags))]
+            lines.append("  unsigned long long lb = 0;")
         lines += body
+        if self.count:
+            lines += [f"  if (lc{k}) atomicAdd(cnt + {k}, lc{k});" for k in range(len(self.loops))]
+            lines += [f"  if (lg{g}) atomicAdd(gcnt + {g}, lg{g});" for g in range(len(self.guard_tags))]
+            lines.append("  if (lb) atomicAdd(bcnt, lb);")
         lines.append("}")
         return Emitted("\n".join(lines) + "\n", self.loops, self.guard_tags, dict(self.mapping), self.inst)
 

@@ -131,7 +131,8 @@ class Executor:
         return g
 
     def stats(self) -> "ExecStats":
-        return ExecStats(self.program, self.plan, self.sparse, self.dims_map)
+        return ExecStats(self.program, self.plan, self.sparse, self.dims_map, operands=self.operands,
+                         dtype=self.dtype, n_out=self.out.numel())
 
     def manifest(self):
         """The reference `ir.Manifest` of this launch (the Program is not
@@ -312,12 +313,16 @@ class ExecStats:
     (per-loop iteration counts, per-parallel-instance work,
     guard failures; sum of per-instance work == total innermost work)."""
 
-    def __init__(self, program: Program, plan, sparse: DeviceTensor, dims: dict):
+    def __init__(self, program: Program, plan, sparse: DeviceTensor, dims: dict, *, operands: dict | None = None,
+                 dtype: str = "f64", n_out: int = 0):
         self.program = program
         self.kernel = program.kernel
         self.params = [int(plan.params[k]) for k in range(8)]
         self._sparse = sparse
         self._dims = dims
+        self._operands = operands
+        self._dtype = dtype
+        self._n_out = n_out
 
     def manifest(self):
         """The `ir.Manifest` (parameter layout + dims) of this execution."""
@@ -387,17 +392,46 @@ class ExecStats:
                 inst[v["warp"]] = np.diff(slice_leaves)
         return inst, loops, guards
 
+    @cached_property
+    def _ir_counted(self) -> dict:
+        """Every loop's iteration count, guard failures and body visits of the
+        statement's ImperativeIR (irlower.lower_ir), counted on the device by
+        a counting launch of the generic kernel into a scratch output: the
+        table kernels do not keep per-loop counters, and the IR visits the
+        same points (tests/test_gpu_irpath.py)."""
+        from . import generic
+
+        if self._operands is None:
+            return {}
+        gp = generic.make_program(self.program.stmt)
+        if not gp.schedule_honoured:
+            return {}
+        dev = self._sparse.device
+        scratch = torch.empty(max(1, self._n_out), dtype=torch_dtype(self._dtype), device=dev)
+        return generic.launch(gp, self._operands, scratch, self._dtype, _cur_stream(dev), count=True)
+
     @property
     def instance_work(self) -> dict:
         return self._computed[0]
 
     @property
     def loop_counts(self) -> dict:
-        return self._computed[1]
+        """Iterations of every loop of the schedule: the
+        parallel loops from the launch partition, the others counted on the
+        device (`_ir_counted`, run the first time this is read)."""
+        out = dict(self._ir_counted.get("loops", {}))
+        out.update(self._computed[1])
+        return out
 
     @property
     def guard_failures(self) -> dict:
-        return self._computed[2]
+        out = dict(self._ir_counted.get("guards", {}))
+        out.update(self._computed[2])
+        return out
+
+    @property
+    def body_visits(self):
+        return self._ir_counted.get("body")
 
     def work(self, var: str) -> np.ndarray:
         return self.instance_work[var]

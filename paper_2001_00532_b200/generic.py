@@ -291,7 +291,7 @@ class _Gen:
         odims = [self.ext[v] for v in self.lhs]
         for v, n in zip(self.lhs, odims):
             oidx = f"({oidx}) * {n}LL + v_{v}"
-        lines.append(ind(d) + f"if (prod != (T)0) atomicAdd(out + ({oidx}), prod);")
+        lines.append(ind(d) + f"atomicAdd(out + ({oidx}), prod);")  # no zero shortcut: 0*inf stays NaN
         for _ in rest:
             d -= 1
             lines.append(ind(d) + "}")

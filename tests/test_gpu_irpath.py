@@ -127,3 +127,25 @@ def test_format_program_of_table_kernel(cuda):
     assert prog.kind == "spmm"
     text = _spindle.ir.format_program(prog.ir({"A": (40, 50), "B": (50, 24)}))
     assert "parallel(GPUBlock, IgnoreRaces)" in text and "search_segment(A2_pos" in text
+
+
+@pytest.mark.parametrize("name", ["A2", "A4", "A6", "K7", "K9", "A1"])
+def test_table_kernel_stats_count_every_loop(cuda, name):
+    """ExecStats of a table kernel reports every loop of the schedule (the
+    device-counted IR), and the body visits equal the stored work."""
+    e = corpus.BY_NAME[name]
+    params = irtools.small_params(e)
+    if "{NNZ_PER_THREAD}" in e.schedule:
+        params.update(NNZ_PER_TB=64, NNZ_PER_WARP=32, NNZ_PER_THREAD=1)  # the table's W == 32*T
+    stmt = corpus.build(name, **params)
+    prog = lower(stmt)
+    assert prog.kind != "generic"
+    ins = irtools.inputs(e, np.random.default_rng(2))
+    got, stats = _run(prog, ins)
+    assert rel_err(got, irtools.dense_eval(stmt, ins)) <= 1e-10
+    loops = stats.loop_counts
+    for v in stmt.forest_names():
+        assert any(k == v or k.startswith(v) for k in loops), (v, loops)
+    sp = ins["A"] if "A" in ins and not isinstance(ins["A"], np.ndarray) else ins["B"]
+    width = irtools.WIDTH if e.expr in (corpus.SPMM, corpus.MTTKRP, corpus.SDDMM) else 1
+    assert stats.body_visits == len(sp.vals) * width

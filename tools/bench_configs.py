@@ -14,6 +14,7 @@ launch.  Compulsory bytes and flop conventions: SURVEY.md §8(d).
 from __future__ import annotations
 
 import argparse
+import os
 import json
 import math
 import statistics
@@ -62,6 +63,22 @@ def pick(schedules, args):
     return [(s[0], {**s[1], **extra}) for s in schedules if not only or s[0] in only]
 
 
+CPU = {}  # last oracle timing: {"cpu_s", "cpu_gflops", "cpu_threads"}
+
+
+def timed_oracle(fn, flops):
+    """Run the CPU restatement (the parity reference) and time it: with
+    --cpu-time it is the -march=native OpenMP build on all host threads
+    (BASELINE.md §4), reported as the config's CPU baseline."""
+    t0 = time.perf_counter()
+    want = fn()
+    dt = time.perf_counter() - t0
+    CPU.clear()
+    CPU.update({"cpu_s": round(dt, 3), "cpu_gflops": round(flops / dt / 1e9, 2),
+                "cpu_threads": int(os.environ.get("OMP_NUM_THREADS", "0") or 0)})
+    return want
+
+
 def rel_err(got: np.ndarray, want: np.ndarray) -> float:
     if want.size == 0:
         return 0.0
@@ -78,6 +95,8 @@ def record(cfg, name, prog, ts, flops, cbytes, err, tol, extra=None):
     }
     if extra:
         rec.update(extra)
+    if err is not None and CPU:
+        rec.update(CPU)
     print(json.dumps(rec), flush=True)
     return rec
 
@@ -91,7 +110,7 @@ def run_spmv(cfg, A, dtype, schedules, args):
     Ad = DeviceTensor.from_arrays((A.M, A.N), "ds", {1: A.pos}, {1: A.crd}, vals, device=dev, dtype=dtype)
     xd = DeviceTensor.dense(x, device=dev, dtype=dtype)
     out = torch.empty(A.M, dtype=Ad.vals.dtype, device=dev)
-    want = O.spmv(A.pos, A.crd, vals, x) if not args.no_parity else None
+    want = timed_oracle(lambda: O.spmv(A.pos, A.crd, vals, x), 2.0 * A.nnz) if not args.no_parity else None
     cb = (4 + es) * A.nnz + 4 * (A.M + 1) + es * A.N + es * A.M
     for name, params in pick(schedules, args):
         prog = lower(corpus.build(name, **params))
@@ -108,7 +127,7 @@ def run_spmm(cfg, A, schedules, args, ncols=128):
     Ad = DeviceTensor.from_arrays((A.M, A.N), "ds", {1: A.pos}, {1: A.crd}, vals, device=dev, dtype="f32")
     Bd = DeviceTensor.dense(B, device=dev, dtype="f32")
     out = torch.empty(A.M * ncols, dtype=torch.float32, device=dev)
-    want = O.spmm(A.pos, A.crd, vals, B) if not args.no_parity else None
+    want = timed_oracle(lambda: O.spmm(A.pos, A.crd, vals, B), 2.0 * A.nnz * ncols) if not args.no_parity else None
     cb = 8 * A.nnz + 4 * (A.M + 1) + 4 * A.N * ncols + 4 * A.M * ncols
     for name, params in pick(schedules, args):
         prog = lower(corpus.build(name, **params))
@@ -128,7 +147,7 @@ def run_sddmm(cfg, A, schedules, args, K=256):
     Cd = DeviceTensor.dense(Cm, device=dev, dtype="f32")
     Dd = DeviceTensor.dense(Dm, device=dev, dtype="f32")
     out = torch.empty(A.nnz, dtype=torch.float32, device=dev)
-    want = O.sddmm(A.pos, A.crd, vals, Cm, Dm) if not args.no_parity else None
+    want = timed_oracle(lambda: O.sddmm(A.pos, A.crd, vals, Cm, Dm), 2.0 * A.nnz * K) if not args.no_parity else None
     cb = 8 * A.nnz + 4 * (A.M + 1) + 4 * A.M * K + 4 * A.N * K + 4 * A.nnz
     for name, params in pick(schedules, args):
         prog = lower(corpus.build(name, **params))
@@ -153,7 +172,8 @@ def run_csf(cfg, T, schedules, args, R=32):
     cd = DeviceTensor.dense(c, device=dev, dtype="f32")
     idx_bytes = 8 * nnz + 8 * F + 8 * S + 16
     info = {"S": S, "F": F, "nnz": nnz}
-    want_m = O.mttkrp(T.dims, T.pos, T.crd, vals, Cm, Dm) if not args.no_parity else None
+    want_m = (timed_oracle(lambda: O.mttkrp(T.dims, T.pos, T.crd, vals, Cm, Dm), 3.0 * nnz * R)
+              if not args.no_parity else None)
     out = torch.empty(I * R, dtype=torch.float32, device=dev)
     for name, params in pick(schedules["mttkrp"], args):
         prog = lower(corpus.build(name, **params))
@@ -162,7 +182,7 @@ def run_csf(cfg, T, schedules, args, R=32):
         err = rel_err(out.cpu().numpy().reshape(I, R), want_m) if want_m is not None else None
         record(cfg, f"{name} {params}", prog, ts, 3.0 * nnz * R, idx_bytes + 3 * (I * R * 4), err, 1e-3, info)
     J = T.dims[1]
-    want_t = O.ttv(T.dims, T.pos, T.crd, vals, c) if not args.no_parity else None
+    want_t = timed_oracle(lambda: O.ttv(T.dims, T.pos, T.crd, vals, c), 2.0 * nnz) if not args.no_parity else None
     out2 = torch.empty(I * J, dtype=torch.float32, device=dev)
     for name, params in pick(schedules["ttv"], args):
         prog = lower(corpus.build(name, **params))
@@ -182,7 +202,11 @@ def main():
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--only", default="", help="comma list of schedule names to run (default all)")
     ap.add_argument("--params", default="", help="K=V,... schedule constants merged into the picked schedules")
+    ap.add_argument("--cpu-time", action="store_true",
+                    help="time the CPU restatement with the -march=native build (BASELINE.md §4)")
     args = ap.parse_args()
+    if args.cpu_time:
+        print("# cpu baseline: " + O.use_native(), file=sys.stderr, flush=True)
     PEAK = hbm_peak()
     FLUSH = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     cfgs = [int(c) for c in args.cfg.split(",")]
