@@ -71,3 +71,53 @@ def test_two_rank_gloo_shards_and_collectives():
     res = sorted(q.get(timeout=5) for _ in range(2))
     assert res == [(0, True, True), (1, True, True)]
     assert all(p.exitcode == 0 for p in procs)
+
+
+def _heavy_worker(rank: int, world: int, port: int, q):
+    sys.path.insert(0, str(ROOT))
+    sys.path.insert(0, str(ROOT / "tests"))
+    import torch.distributed as dist
+
+    from oracle import oracle as O
+    from paper_2001_00532_b200 import synth
+    from paper_2001_00532_b200.partition import csf_shards, reduce_partials
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(3)
+        n, nnz = 128, 30_000
+        heavy = int(0.3 * nnz)
+        keys = np.sort(np.concatenate([rng.choice(n * n, heavy, replace=False),
+                                       rng.choice((n - 1) * n * n, nnz - heavy, replace=False) + n * n]))
+        T = synth.csf_from_keys(keys.astype(np.int64), rng.uniform(-1, 1, nnz), 7)
+        C = synth.dense((n, 8), seed=8)
+        D = synth.dense((n, 8), seed=9)
+        shards = csf_shards(T.pos, T.crd, T.vals, world, exact=True)
+        split = sum(1 for s in shards if len(s.crd[0]) and s.crd[0][0] == 0)
+        part = shards[rank]
+        partial = torch.from_numpy(O.mttkrp(T.dims, part.pos, part.crd, part.vals, C, D))
+        tot = reduce_partials(partial).numpy()
+        ok = np.allclose(tot, O.mttkrp(T.dims, T.pos, T.crd, T.vals, C, D), rtol=1e-10, atol=1e-12)
+        q.put((rank, bool(ok), split))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_four_rank_gloo_heavy_slice_reduction():
+    """one slice with 30 % of the leaves, leaf-exact shards
+    over 4 ranks -> the slice spans two ranks and their partial rows are
+    summed by reduce_partials (the all-reduce the GPU path runs over NCCL)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_heavy_worker, args=(r, 4, port, q)) for r in range(4)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+    res = sorted(q.get(timeout=5) for _ in range(4))
+    assert [r[:2] for r in res] == [(r, True) for r in range(4)]
+    assert res[0][2] >= 2
+    assert all(p.exitcode == 0 for p in procs)
