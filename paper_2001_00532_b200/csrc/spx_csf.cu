@@ -943,10 +943,8 @@ int run_mttkrp(int kid, const Args& a) {
       // 16 B leaf copies need every quarter chunk to start on a 4-leaf boundary
       auto kern = W % 16 == 0 ? mttkrp_quarter_kernel<true> : mttkrp_quarter_kernel<false>;
       static bool carve = [] {
-        cudaFuncSetAttribute(mttkrp_quarter_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                             SPX_MQ_CARVEOUT);
-        cudaFuncSetAttribute(mttkrp_quarter_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                             SPX_MQ_CARVEOUT);
+        for (auto k : {mttkrp_quarter_kernel<true>, mttkrp_quarter_kernel<false>})
+          cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, SPX_MQ_CARVEOUT);
         return true;
       }();
       (void)carve;

@@ -24,13 +24,17 @@ from paper_2001_00532_b200.formats import DeviceTensor  # noqa: E402
 from paper_2001_00532_b200.partition import csf_shards, csr_shards  # noqa: E402
 
 
-def heavy_slice_csf(bits=7, nnz=200_000, frac=0.3, seed=3):
-    """CSF whose slice i=0 holds `frac` of the leaves."""
+HEAVY = 256  # the middle slice, so the leaf-exact cut at 50 % falls inside it
+
+
+def heavy_slice_csf(bits=9, nnz=200_000, frac=0.3, seed=3):
+    """CSF whose slice i=HEAVY holds `frac` of the leaves (the rest spread evenly)."""
     rng = np.random.default_rng(seed)
     n = 1 << bits
     heavy = int(nnz * frac)
-    k0 = rng.choice(n * n, heavy, replace=False)  # (k, l) pairs of slice 0
-    rest = rng.choice((n - 1) * n * n, nnz - heavy, replace=False) + n * n
+    k0 = rng.choice(n * n, heavy, replace=False) + HEAVY * n * n  # (k, l) pairs of the heavy slice
+    rest = rng.choice((n - 1) * n * n, nnz - heavy, replace=False)
+    rest = np.where(rest >= HEAVY * n * n, rest + n * n, rest)  # skip the heavy slice
     keys = np.sort(np.concatenate([k0, rest]).astype(np.int64))
     vals = rng.uniform(-1, 1, nnz)
     return synth.csf_from_keys(keys, vals, bits)
@@ -53,7 +57,7 @@ def test_mttkrp_leaf_exact_shards_sum_to_full(cuda, world, name):
     total = torch.zeros(n * R, dtype=torch.float32, device=cuda)
     shards = csf_shards(T.pos, T.crd, v, world, exact=True)
     assert sum(len(s.vals) for s in shards) == len(v)
-    split = sum(1 for s in shards if len(s.crd[0]) and s.crd[0][0] == 0)
+    split = sum(1 for s in shards if HEAVY in set(s.crd[0].tolist()))
     assert split >= 2  # the heavy slice spans ranks: the reduction has work to do
     for s in shards:
         Bd = DeviceTensor.from_arrays(T.dims, "sss", s.pos, s.crd, s.vals, device=cuda, dtype="f32")
