@@ -565,7 +565,13 @@ constexpr int kQThreads = SPX_MQ_THREADS;
 #ifndef SPX_MQ_SMWIN
 #define SPX_MQ_SMWIN 1  // fiber window in shared memory (else per-lane registers + width-8 shuffles)
 #endif
-constexpr int kQSlotBytes = 32 * 4 * 2;   // 32 crd + 32 vals (fp32)
+#ifndef SPX_MQ_QB
+#define SPX_MQ_QB 16  // leaves per quarter per batch with 16 B copies (8: half the lanes copy)
+#endif
+// a ring slot: QB coordinates then QB values per quarter (fp32)
+template <int QB>
+constexpr int q_slot_bytes() { return 4 * QB * 8; }
+constexpr int kQSlotBytes = q_slot_bytes<8>();
 
 __device__ __forceinline__ int4 lds_i4(uint32_t a) {
   int4 r;
@@ -601,11 +607,16 @@ __global__ void __launch_bounds__(kQThreads, SPX_MQ_MINB) mttkrp_quarter_kernel(
   // rowb = 128 (bytes per C / D row) arrives as a parameter so that row
   // addresses stay one IMAD.WIDE.U32 (a literal 128 is strength-reduced to
   // a three-instruction shift-and-add)
+  // QB leaves per quarter per batch: AL16 uses SPX_MQ_QB (16: every lane
+  // issues one 16 B copy per batch, no lane predicate), else 8 (4 B copies)
+  constexpr int QB = AL16 ? SPX_MQ_QB : 8;
+  constexpr int kSlot = q_slot_bytes<QB>();
+  constexpr int kValOff = 4 * QB * 4;  // values follow the four quarters' coordinates
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qw = lane >> 3, ql = lane & 7;
   const unsigned qmask = 0xFFu << (qw * 8);
-  unsigned char* ring = smem_raw + (size_t)warp * (kQRing * kQSlotBytes);
+  unsigned char* ring = smem_raw + (size_t)warp * (kQRing * kSlot);
   const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
   const uint64_t pol_s = l2_evict_first();
 #if SPX_MQ_SMWIN
@@ -615,17 +626,19 @@ __global__ void __launch_bounds__(kQThreads, SPX_MQ_MINB) mttkrp_quarter_kernel(
   const char* __restrict__ Cl = reinterpret_cast<const char*>(Cm) + ql * 16;
   const char* __restrict__ Dl = reinterpret_cast<const char*>(Dm) + ql * 16;
   float* __restrict__ Al = A + ql * 4;
-  // the quarter's 8 leaf coordinates / values of a slot (broadcast LDS.128)
-  const int rd_off = qw * 32;
-  // AL16: lanes 0-3 of a quarter copy 16 B each -- (coordinates | values) x (leaves 0-3 | 4-7)
-  const int cp_h = ql & 1, cp_which = (ql >> 1) & 1;
-  const uint32_t cp_dst = (uint32_t)(cp_which * 128 + qw * 32 + cp_h * 16);
+  // the quarter's QB leaf coordinates / values of a slot (broadcast LDS.128)
+  const int rd_off = qw * QB * 4;
+  // AL16: QB/2 lanes of a quarter copy 16 B each -- (coordinates | values) x QB/4 chunks of 4 leaves
+  constexpr int kChunks = QB / 4;
+  const int cp_h = ql % kChunks, cp_which = (ql / kChunks) & 1;
+  const bool cp_lane = ql < 2 * kChunks;
+  const uint32_t cp_dst = (uint32_t)(cp_which * kValOff + qw * QB * 4 + cp_h * 16);
   const char* cp_src = cp_which ? reinterpret_cast<const char*>(vals) : reinterpret_cast<const char*>(crd2);
   const int Wq = W >> 2;
   for (int q = blockIdx.x * nw + warp; q < nchunks; q += gridDim.x * nw) {
     const int c0 = q * W, c1 = min(c0 + W, nnz);
     const int a = min(c0 + qw * Wq, c1), b = min(a + Wq, c1);
-    const int nbw = (min(Wq, c1 - c0) + 7) >> 3;  // batches of 8 leaves (quarter 0 has the most)
+    const int nbw = (min(Wq, c1 - c0) + QB - 1) / QB;  // batches of QB leaves (quarter 0 has the most)
     // issue batch bi into ring slot `slot`
     // AL16: this lane's next 16 B source and how many of its leaves remain
     const char* isrc = cp_src + (size_t)(a + cp_h * 4) * 4;
@@ -633,12 +646,12 @@ __global__ void __launch_bounds__(kQThreads, SPX_MQ_MINB) mttkrp_quarter_kernel(
     auto issue = [&](int bi, uint32_t slot) {
       if (bi < nbw) {
         if constexpr (AL16) {
-          if (ql < 4) {
+          if (cp_lane) {
             const int nv = max(0, min(4, irem));
             cp_async16_zfill(ring_s + slot + cp_dst, nv ? isrc : cp_src, nv * 4, pol_s);
           }
-          isrc += 32;
-          irem -= 8;
+          isrc += QB * 4;
+          irem -= QB;
         } else {
           const int p = a + bi * 8 + ql;
           const bool ok = p < b;
@@ -648,9 +661,9 @@ __global__ void __launch_bounds__(kQThreads, SPX_MQ_MINB) mttkrp_quarter_kernel(
       }
       cp_async_commit();
     };
-    uint32_t rslot = 0, islot = (kQRing - 1) * kQSlotBytes;
+    uint32_t rslot = 0, islot = (kQRing - 1) * kSlot;
 #pragma unroll
-    for (int bi = 0; bi < kQRing - 1; ++bi) issue(bi, bi * kQSlotBytes);
+    for (int bi = 0; bi < kQRing - 1; ++bi) issue(bi, bi * kSlot);
     const bool live = a < b;
     int f = live ? __ldg(chunkF + q * 4 + qw) : 0;
     int s = live ? __ldg(chunkS + q * 4 + qw) : 0;
@@ -736,16 +749,16 @@ __global__ void __launch_bounds__(kQThreads, SPX_MQ_MINB) mttkrp_quarter_kernel(
 #pragma unroll 1
     for (int bi = 0; bi < nbw; ++bi) {
       issue(bi + kQRing - 1, islot);
-      islot = islot == (kQRing - 1) * kQSlotBytes ? 0 : islot + kQSlotBytes;
+      islot = islot == (kQRing - 1) * kSlot ? 0 : islot + kSlot;
       cp_async_wait<kQRing - 1>();
       __syncwarp();
       const uint32_t sl = ring_s + rslot + rd_off;
-      rslot = rslot == (kQRing - 1) * kQSlotBytes ? 0 : rslot + kQSlotBytes;
+      rslot = rslot == (kQRing - 1) * kSlot ? 0 : rslot + kSlot;
 #pragma unroll
-      for (int h = 0; h < 2; ++h, pp += 4) {
+      for (int h = 0; h < QB / 4; ++h, pp += 4) {
         const int4 l4 = lds_i4(sl + h * 16);
         const float4 d0 = SPX_DR(l4.x), d1 = SPX_DR(l4.y), d2 = SPX_DR(l4.z), d3 = SPX_DR(l4.w);
-        const float4 v4 = lds_f4(sl + 128 + h * 16);
+        const float4 v4 = lds_f4(sl + kValOff + h * 16);
         if (pp + 4 <= fend) {  // leaves pp..pp+3 lie in fiber f (zero-filled past b)
           SPX_QF(v4.x, d0);
           SPX_QF(v4.y, d1);
@@ -939,12 +952,19 @@ int run_mttkrp(int kid, const Args& a) {
                                                                          (int)c.S, (int)c.F, (int)Wq);
       count_launch();
       if (int e = check_cuda(cudaGetLastError(), "ttv_prep_kernel")) return e;
-      const size_t smem = (size_t)(kQThreads / 32) * kQRing * kQSlotBytes;
+      const size_t smem = (size_t)(kQThreads / 32) * kQRing * (W % 16 == 0 ? q_slot_bytes<SPX_MQ_QB>() : kQSlotBytes);
       // 16 B leaf copies need every quarter chunk to start on a 4-leaf boundary
       auto kern = W % 16 == 0 ? mttkrp_quarter_kernel<true> : mttkrp_quarter_kernel<false>;
       static bool carve = [] {
-        for (auto k : {mttkrp_quarter_kernel<true>, mttkrp_quarter_kernel<false>})
-          cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, SPX_MQ_CARVEOUT);
+        // the smallest shared-memory carveout that holds SPX_MQ_MINB CTAs
+        // (ring + fiber windows + 1 KB reserved each): the rest stays L1 for D
+        for (int al = 0; al < 2; ++al) {
+          const size_t dyn = (size_t)(kQThreads / 32) * kQRing * (al ? q_slot_bytes<SPX_MQ_QB>() : kQSlotBytes);
+          const size_t need = (size_t)SPX_MQ_MINB * (dyn + 4096 + 1024);
+          const int pct = std::max<int>(SPX_MQ_CARVEOUT, (int)((need * 100 + 228 * 1024 - 1) / (228 * 1024)));
+          cudaFuncSetAttribute(al ? mttkrp_quarter_kernel<true> : mttkrp_quarter_kernel<false>,
+                               cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+        }
         return true;
       }();
       (void)carve;
