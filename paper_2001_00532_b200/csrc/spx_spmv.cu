@@ -350,6 +350,9 @@ __global__ void __launch_bounds__(kMaxThreads, 2) spmv_nnz_kernel(const int32_t*
 // CTA barrier and no carry fix-up.  fp64 sums of a row split across warps
 // may differ in the last bits from run to run (atomic order).
 constexpr int kWarpPos = 320;  // pos entries staged per warp
+#ifndef SPX_SPMV_CARVEOUT
+#define SPX_SPMV_CARVEOUT 20  // percent of 228 KB: 4 CTAs x 8 warps x 1.25 KB of pos slices fit the 64 KB config
+#endif
 
 // tuning knob: 3 CTAs/SM forces 40 registers and spills (cfg5 1.32 vs 1.15 ms)
 #ifndef SPX_SPMV_MINB
@@ -364,8 +367,10 @@ __global__ void __launch_bounds__(kMaxThreads, SPX_SPMV_MINB) spmv_nnz_atomic_ke
     const int32_t* __restrict__ pos, const int32_t* __restrict__ crd, const T* __restrict__ vals,
     const T* __restrict__ x, T* __restrict__ y, int64_t M, int64_t nnz, int64_t W, int tpt_rt,
     const int32_t* __restrict__ first, int64_t xlen = 0) {
-  __shared__ int32_t s_pos_all[kMaxWarps][kWarpPos];
+  // dynamic shared memory: [x (XS only)] [pos slices, kWarpPos per warp of this CTA] -- sized by
+  // the CTA's actual warps, so the carveout leaves the rest of the SM's 256 KB to L1 (x gathers)
   extern __shared__ __align__(16) unsigned char smem_x[];
+  int32_t* s_pos_all = reinterpret_cast<int32_t*>(smem_x + (XS ? ((size_t)xlen * sizeof(T) + 15) / 16 * 16 : 0));
   const T* __restrict__ xr = x;
   if constexpr (XS) {
     T* sx = reinterpret_cast<T*>(smem_x);
@@ -375,7 +380,7 @@ __global__ void __launch_bounds__(kMaxThreads, SPX_SPMV_MINB) spmv_nnz_atomic_ke
   }
   const int tpt = TPT > 0 ? TPT : tpt_rt;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int32_t* s_pos = s_pos_all[warp];
+  int32_t* s_pos = s_pos_all + warp * kWarpPos;
   const int q = (int)blockIdx.x * (int)(blockDim.x >> 5) + warp;  // warp chunk
   const int q0 = (int)((int64_t)q * W);
   if ((int64_t)q0 >= nnz) return;
@@ -499,20 +504,31 @@ int segsum_atomic(const int32_t* pos, const int32_t* crd, const T* vals, const T
                   int64_t xlen = 0) {
   const int threads = (int)(TB / TPT);
   const unsigned g = (unsigned)(nnz == 0 ? 1 : ceil_div(nnz, TB));
+  const size_t pbytes = (size_t)((threads + 31) / 32) * kWarpPos * sizeof(int32_t);
   // x in shared memory when it is short (<= 16 KB) and no larger than the
   // (crd, vals) bytes a CTA streams (every CTA stages all of x)
   const size_t xbytes = (size_t)xlen * sizeof(T);
   if (TPT == 8 && xlen > 0 && xbytes <= 16384 && (size_t)TB * (4 + sizeof(T)) >= xbytes) {
-    spmv_nnz_atomic_kernel<T, 8, true><<<g, threads, xbytes, st>>>(pos, crd, vals, x, y, nseg, nnz, W, 8, first, xlen);
+    const size_t sm = (xbytes + 15) / 16 * 16 + pbytes;
+    spmv_nnz_atomic_kernel<T, 8, true><<<g, threads, sm, st>>>(pos, crd, vals, x, y, nseg, nnz, W, 8, first, xlen);
     count_launch();
     return check_cuda(cudaGetLastError(), "spmv_nnz_atomic_kernel");
   }
+  static bool carve = [] {  // shared memory for the resident CTAs' pos slices; the rest is L1
+    for (auto k : {spmv_nnz_atomic_kernel<T, 4>, spmv_nnz_atomic_kernel<T, 8>, spmv_nnz_atomic_kernel<T, 16>,
+                   spmv_nnz_atomic_kernel<T, 0>})
+      cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, SPX_SPMV_CARVEOUT);
+    return true;
+  }();
+  (void)carve;
   switch (TPT) {
-    case 4: spmv_nnz_atomic_kernel<T, 4><<<g, threads, 0, st>>>(pos, crd, vals, x, y, nseg, nnz, W, 4, first); break;
-    case 8: spmv_nnz_atomic_kernel<T, 8><<<g, threads, 0, st>>>(pos, crd, vals, x, y, nseg, nnz, W, 8, first); break;
-    case 16: spmv_nnz_atomic_kernel<T, 16><<<g, threads, 0, st>>>(pos, crd, vals, x, y, nseg, nnz, W, 16, first); break;
+    case 4: spmv_nnz_atomic_kernel<T, 4><<<g, threads, pbytes, st>>>(pos, crd, vals, x, y, nseg, nnz, W, 4, first); break;
+    case 8: spmv_nnz_atomic_kernel<T, 8><<<g, threads, pbytes, st>>>(pos, crd, vals, x, y, nseg, nnz, W, 8, first); break;
+    case 16:
+      spmv_nnz_atomic_kernel<T, 16><<<g, threads, pbytes, st>>>(pos, crd, vals, x, y, nseg, nnz, W, 16, first);
+      break;
     default:
-      spmv_nnz_atomic_kernel<T, 0><<<g, threads, 0, st>>>(pos, crd, vals, x, y, nseg, nnz, W, (int)TPT, first);
+      spmv_nnz_atomic_kernel<T, 0><<<g, threads, pbytes, st>>>(pos, crd, vals, x, y, nseg, nnz, W, (int)TPT, first);
   }
   count_launch();
   return check_cuda(cudaGetLastError(), "spmv_nnz_atomic_kernel");
