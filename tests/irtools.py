@@ -128,3 +128,92 @@ def space_input(fmt: str):
         return vals
     coo = T.CooTensor(SPACE, [((i, j), float(vals[i, j])) for i in range(8) for j in range(9)])
     return T.pack(coo, T.parse_format(fmt))
+
+
+# -- random schedules on the corpus expressions (with parallel tags) ------------
+
+EXPRS = [
+    ("y(i) = A(i,j) * x(j)", {"A": "ds", "x": "d"}, "A"),
+    ("y(i) = A(i,j) * x(j)", {"A": "ss", "x": "d"}, "A"),
+    ("C(i,k) = A(i,j) * B(j,k)", {"A": "ds", "B": "dd"}, "A"),
+    ("A(i,j) = B(i,j) * C(i,k) * D(j,k)", {"B": "ds", "C": "dd", "D": "dd"}, "B"),
+    ("A(i,j) = B(i,j,k) * c(k)", {"B": "sss", "c": "d"}, "B"),
+    ("A(i,j) = B(i,k,l) * C(k,j) * D(l,j)", {"B": "sss", "C": "dd", "D": "dd"}, "B"),
+]
+
+UNITS = ["GPUBlock", "GPUWarp", "GPUThread", "CPUThread"]
+RACES = ["IgnoreRaces", "Atomics", "NoRaces"]
+
+
+def random_schedule(rng, expr, fmts, sparse, max_steps=5, tags=True):
+    """A random valid composition of split/divide/fuse/reorder/pos/coord (pos
+    over the sparse operand) plus random parallel tags on the result."""
+    stmt = S.concretize(N.parse_assignment(expr), dict(fmts))
+    acc = next(a for a in stmt.assignment.input_accesses() if a.tensor == sparse)
+    steps = []
+    n_new = 0
+    for _ in range(int(rng.integers(0, max_steps + 1))):
+        forest = stmt.forest_names()
+        op = rng.choice(["split", "divide", "fuse", "reorder", "pos", "coord", "bound"])
+        v = str(rng.choice(forest))
+        try:
+            if op == "split":
+                new = S.split(stmt, v, f"s{n_new}", f"t{n_new}", int(rng.integers(1, 9)))
+            elif op == "divide":
+                new = S.divide(stmt, v, f"s{n_new}", f"t{n_new}", int(rng.integers(1, 6)))
+            elif op == "fuse":
+                k = forest.index(v)
+                if k + 1 >= len(forest):
+                    continue
+                new = S.fuse(stmt, v, forest[k + 1], f"f{n_new}")
+            elif op == "reorder":
+                if len(forest) < 2:
+                    continue
+                lo = int(rng.integers(0, len(forest) - 1))
+                hi = int(rng.integers(lo + 2, len(forest) + 1))
+                run = list(forest[lo:hi])
+                rng.shuffle(run)
+                new = S.reorder(stmt, run)
+            elif op == "pos":
+                new = S.pos(stmt, v, f"p{n_new}", acc)
+            elif op == "coord":
+                new = S.coord(stmt, v, f"c{n_new}")
+            else:
+                continue
+        except (_spindle.errors.SchedulingError, _spindle.errors.GraphError):
+            continue
+        stmt = new
+        steps.append(f"{op}({v})")
+        n_new += 1
+    if tags:
+        used = set()
+        for v in stmt.forest_names():
+            if rng.random() < 0.5:
+                unit = str(rng.choice([u for u in UNITS if u not in used] or UNITS))
+                race = str(rng.choice(RACES))
+                try:
+                    stmt = S.parallelize(stmt, v, unit, race)
+                    used.add(unit)
+                    steps.append(f"parallelize({v},{unit},{race})")
+                except (_spindle.errors.SchedulingError, _spindle.errors.RaceError):
+                    pass
+    return stmt, steps
+
+
+def expr_inputs(expr, fmts, rng, small=True):
+    """Random operands for one of EXPRS (small dims, density 0.2-0.3)."""
+    asg = N.parse_assignment(expr)
+    ext, ins = {}, {}
+    for acc in asg.input_accesses():
+        if acc.tensor in ins:
+            continue
+        dims = []
+        for v in acc.vars:
+            ext.setdefault(v.name, int(rng.integers(3, 9)) if small else int(rng.integers(20, 60)))
+            dims.append(ext[v.name])
+        lv = fmts.get(acc.tensor, "d" * len(dims))
+        if "s" in lv:
+            ins[acc.tensor] = sparse(tuple(dims), lv, 0.3, rng)
+        else:
+            ins[acc.tensor] = rng.uniform(-1, 1, tuple(dims))
+    return ins

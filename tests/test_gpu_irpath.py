@@ -149,3 +149,27 @@ def test_table_kernel_stats_count_every_loop(cuda, name):
     sp = ins["A"] if "A" in ins and not isinstance(ins["A"], np.ndarray) else ins["B"]
     width = irtools.WIDTH if e.expr in (corpus.SPMM, corpus.MTTKRP, corpus.SDDMM) else 1
     assert stats.body_visits == len(sp.vals) * width
+
+
+@pytest.mark.parametrize("k", range(len(irtools.EXPRS)))
+def test_random_tagged_schedules_gpu(cuda, k):
+    """Random compositions of the corpus expressions with random
+    GPUBlock / GPUWarp / GPUThread / CPUThread tags and race strategies: the
+    generated kernels map whatever nesting the tags produce onto the hardware
+    and still match dense_eval (fp64, 1e-10)."""
+    import warnings
+
+    expr, fmts, sp = irtools.EXPRS[k]
+    rng = np.random.default_rng(200 + k)
+    done = 0
+    while done < 25:
+        stmt, steps = irtools.random_schedule(rng, expr, fmts, sp)
+        ins = irtools.expr_inputs(expr, fmts, rng)
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore", generic.LoweringFallbackWarning)
+            prog = generic.make_program(stmt)
+        if not prog.schedule_honoured:
+            continue
+        done += 1
+        got, _ = _run(prog, ins)
+        assert rel_err(got, irtools.dense_eval(stmt, ins)) <= 1e-10, (expr, steps)

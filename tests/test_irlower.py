@@ -246,3 +246,22 @@ def test_generic_cases_match_dense_eval():
             ins[acc.tensor], _ = _rand_tensor(tuple(dims), formats.get(acc.tensor, "d" * len(dims)), rng)
         _, got, want, *_ = run_ir(stmt, ins)
         assert np.max(np.abs(got - want) / np.maximum(1.0, np.abs(want))) <= 1e-12, expr
+
+
+@pytest.mark.parametrize("k", range(len(irtools.EXPRS)))
+def test_random_schedules_on_corpus_expressions(k):
+    """Random compositions (with random parallel tags, which must not change
+    the result) of the corpus expressions: IR == dense_eval (fp64)."""
+    expr, fmts, sp = irtools.EXPRS[k]
+    rng = np.random.default_rng(100 + k)
+    done = 0
+    while done < 25:
+        stmt, steps = irtools.random_schedule(rng, expr, fmts, sp)
+        ins = irtools.expr_inputs(expr, fmts, rng)
+        try:
+            _, got, want, *_ = run_ir(stmt, ins)
+        except _spindle.errors.LoweringError:
+            continue  # outside the IR lowering (reported with a warning at lower())
+        done += 1
+        err = np.max(np.abs(got - want) / np.maximum(1.0, np.abs(want))) if want.size else 0.0
+        assert err <= 1e-10, (expr, steps, err)
