@@ -50,6 +50,7 @@ sys.path.insert(0, str(ROOT))
 METRIC = "SpMM/SpMV GFLOP/s and % HBM roofline at 1/2/4/8 B200 vs CPU oracle"
 WORKLOAD = "cfg2: CSR SpMM nnz-split (A.4: pos+fuse+split), R-MAT scale 20, 1048576^2, 50M nnz x dense N=128, fp32"
 FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback
+MTTKRP_FIBER_WEIGHT = 8.0  # cfg4 shard balance: leaves + w * fibers (tools/bench_shards.py --exact --fiber-weight)
 
 
 def parse():
@@ -394,7 +395,10 @@ def secondary_mttkrp(args, ctx) -> dict:
     Cm = synth.dense((T.dims[1], R), seed=401, dtype=np.float32)
     Dm = synth.dense((T.dims[2], R), seed=402, dtype=np.float32)
     if world > 1:
-        sh = csf_shards(T.pos, T.crd, vals32, world, exact=True)[rank]
+        # leaf-exact cuts balancing leaves + 8 * fibers: the nnz-split kernel pays a
+        # fixed cost per fiber end (projected 8-GPU speed-up 5.03x -> 5.77x,
+        # profiles/r02_shard_scaling.jsonl)
+        sh = csf_shards(T.pos, T.crd, vals32, world, exact=True, fiber_weight=MTTKRP_FIBER_WEIGHT)[rank]
         pos, crd, vals = sh.pos, sh.crd, sh.vals
     else:
         pos, crd, vals = T.pos, T.crd, vals32
@@ -445,7 +449,8 @@ def secondary_mttkrp(args, ctx) -> dict:
     return {"workload": "cfg4: CSF MTTKRP nnz-split (A.6), 2048^3 bit-skewed, 100M nnz, R=32, fp32",
             "schedule": prog.describe(), "n_gpus": world, "value": round(3.0 * nnz * R / (t_ms * 1e-3) / 1e9, 3),
             "unit": "GFLOP/s", "ms_per_step": round(t_ms, 4), "kernel_ms": round(k_ms, 4), "dtype": "f32",
-            "parallelism": f"leaf-exact CSF shards x{world} + NCCL all-reduce of the partial A" if world > 1
+            "parallelism": f"leaf-exact CSF shards x{world} (leaves + {MTTKRP_FIBER_WEIGHT:g} x fibers balanced) "
+                           "+ NCCL all-reduce of the partial A" if world > 1
             else "1 GPU",
             "roofline": {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
                          "frac": round(ach / hbm, 4), "algorithmic_bytes_per_step": int(cb_sum),

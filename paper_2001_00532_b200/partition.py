@@ -119,9 +119,26 @@ def csf_shards(pos: dict, crd: dict, vals: np.ndarray, ndev: int, exact: bool = 
     """Slice shards by the `divide` rule on the leaves (or leaf-exact shards).
     `fiber_weight` > 0 balances leaves + fiber_weight * fibers instead: the
     nnz-split MTTKRP pays a fixed cost per fiber end, so slices of short
-    fibers cost more per leaf (the same rule on that cost, snapped to slices)."""
+    fibers cost more per leaf (the same rule on that cost, snapped to slices,
+    or cut at exact leaf positions with `exact`)."""
     nnz = len(vals)
     if exact:
+        if fiber_weight > 0 and nnz:
+            # leaf-exact cuts balancing leaves + w * fibers: inside fiber f the
+            # cost of the first p leaves is p + w*(f+1), so the cut for target T
+            # lies in the fiber whose start cost pos2[f] + w*(f+1) is the last <= T
+            pos2 = pos[2].astype(np.int64)
+            F = len(pos2) - 1
+            start_cost = pos2[:-1] + fiber_weight * np.arange(1, F + 1)
+            total = nnz + fiber_weight * F
+            cuts = [0]
+            for g in range(1, ndev):
+                T = g * total / ndev
+                f = max(0, int(np.searchsorted(start_cost, T, side="right")) - 1)
+                p = int(round(T - fiber_weight * (f + 1)))
+                cuts.append(min(max(p, int(pos2[f]), cuts[-1]), int(pos2[f + 1]), nnz))
+            cuts.append(nnz)
+            return [_csf_sub(pos, crd, vals, cuts[g], cuts[g + 1]) for g in range(ndev)]
         chunk = -(-nnz // ndev) if nnz else 0
         return [_csf_sub(pos, crd, vals, min(g * chunk, nnz), min((g + 1) * chunk, nnz)) for g in range(ndev)]
     seg_start = pos[2][pos[1][:-1].astype(np.int64)]

@@ -121,3 +121,29 @@ def test_four_rank_gloo_heavy_slice_reduction():
     assert [r[:2] for r in res] == [(r, True) for r in range(4)]
     assert res[0][2] >= 2
     assert all(p.exitcode == 0 for p in procs)
+
+
+def test_weighted_exact_csf_shards_cover_and_balance():
+    """Leaf-exact shards balancing leaves + w * fibers: contiguous, every leaf
+    exactly once, the weighted cost per shard within one fiber's weight plus
+    one leaf of the ideal, and the partial MTTKRPs sum to the full result."""
+    sys.path.insert(0, str(ROOT))
+    from oracle import oracle as O
+    from paper_2001_00532_b200 import synth
+    from paper_2001_00532_b200.partition import csf_shards
+
+    T = synth.bitskew_csf(8, 120_000, seed=11, cache=False)
+    C = synth.dense((256, 8), seed=12)
+    D = synth.dense((256, 8), seed=13)
+    full = O.mttkrp(T.dims, T.pos, T.crd, T.vals, C, D)
+    pos2 = T.pos[2].astype(np.int64)
+    for G in (2, 3, 8):
+        for w in (0.0, 8.0, 25.0):
+            sh = csf_shards(T.pos, T.crd, T.vals, G, exact=True, fiber_weight=w)
+            assert sum(len(s.vals) for s in sh) == len(T.vals)
+            got = sum(O.mttkrp(T.dims, s.pos, s.crd, s.vals, C, D) for s in sh)
+            assert np.allclose(got, full, rtol=1e-10, atol=1e-12), (G, w)
+            if w:
+                cost = [len(s.vals) + w * len(s.crd[1]) for s in sh]
+                ideal = (len(T.vals) + w * (len(pos2) - 1)) / G
+                assert max(abs(c - ideal) for c in cost) <= 2 * w + 2 + 0.02 * ideal, (G, w, cost, ideal)
