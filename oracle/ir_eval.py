@@ -42,6 +42,42 @@ def _arr(IR, tensors, out, ws, ref):
     return ws[ref.tensor]
 
 
+class Scope:
+    """Block-scoped bindings: Declare binds in the innermost scope, Assign
+    updates the nearest enclosing binding (C semantics, as the emitted
+    CUDA)."""
+
+    def __init__(self, parent=None):
+        self.vars = {}
+        self.parent = parent
+
+    def lookup(self, name):
+        s = self
+        while s is not None:
+            if name in s.vars:
+                return s.vars[name]
+            s = s.parent
+        raise IRError(f"undeclared variable {name!r}")
+
+    def assign(self, name, value):
+        s = self
+        while s is not None:
+            if name in s.vars:
+                s.vars[name] = value
+                return
+            s = s.parent
+        raise IRError(f"assignment to undeclared variable {name!r}")
+
+    def get(self, name, default=None):
+        try:
+            return self.lookup(name)
+        except IRError:
+            return default
+
+    def __getitem__(self, name):
+        return self.lookup(name)
+
+
 def run(program, tensors: Tensors, out, *, visit=None, errors=None):
     """Execute `program` into `out` (a flat float array, zeroed by the
     caller).  Returns (loop_counts, guard_failures, body_visits) Counters.
@@ -62,9 +98,7 @@ def run(program, tensors: Tensors, out, *, visit=None, errors=None):
         if isinstance(e, IR.FloatLit):
             return e.value
         if isinstance(e, IR.VarRef):
-            if e.name not in env:
-                raise IRError(f"undeclared variable {e.name!r}")
-            return env[e.name]
+            return env.lookup(e.name)
         if isinstance(e, IR.DimRef):
             return int(tensors.t[e.tensor][0][e.level])
         if isinstance(e, IR.Load):
@@ -100,23 +134,27 @@ def run(program, tensors: Tensors, out, *, visit=None, errors=None):
 
     def ex(s, env):
         if isinstance(s, IR.Block):
+            inner = Scope(env)
             for x in s.stmts:
-                ex(x, env)
-        elif isinstance(s, IR.Declare):
-            env[s.name] = ev(s.init, env)
+                if isinstance(x, IR.Block):
+                    ex(x, inner)
+                else:
+                    ex1(x, inner)
+        else:
+            ex1(s, env)
+
+    def ex1(s, env):
+        if isinstance(s, IR.Declare):
+            env.vars[s.name] = ev(s.init, env)
         elif isinstance(s, IR.Assign):
-            env[s.name] = ev(s.value, env)
+            env.assign(s.name, ev(s.value, env))
         elif isinstance(s, IR.ForLoop):
             lo, hi = int(ev(s.lo, env)), int(ev(s.hi, env))
             for v in range(lo, hi):
                 loops[s.var] += 1
-                inner = dict(env)
-                inner[s.var] = v
-                ex(s.body, inner)
-                # Track state (Assign to outer names) flows out of the body
-                for k in env:
-                    if k in inner and k != s.var:
-                        env[k] = inner[k]
+                it = Scope(env)
+                it.vars[s.var] = v
+                ex(s.body, it)
         elif isinstance(s, IR.WhileLoop):
             n = 0
             while ev(s.cond, env):
@@ -153,7 +191,7 @@ def run(program, tensors: Tensors, out, *, visit=None, errors=None):
                     r, lo = mid, mid + 1
                 else:
                     hi = mid
-            env[s.result] = r
+            env.vars[s.result] = r
         elif isinstance(s, IR.SearchCoord):
             arr = _arr(IR, tensors, out, ws, s.array)
             lo, hi, key = int(ev(s.lo, env)), int(ev(s.hi, env)), ev(s.key, env)
@@ -163,7 +201,7 @@ def run(program, tensors: Tensors, out, *, visit=None, errors=None):
                     lo = mid + 1
                 else:
                     hi = mid
-            env[s.result] = lo
+            env.vars[s.result] = lo
         elif isinstance(s, IR.AssertExtent):
             a, b = ev(s.actual, env), ev(s.expected, env)
             if a != b:
@@ -175,5 +213,5 @@ def run(program, tensors: Tensors, out, *, visit=None, errors=None):
         else:
             raise IRError(f"unknown statement {s!r}")
 
-    ex(program.body, {})
+    ex(program.body, Scope())
     return loops, guards, visits

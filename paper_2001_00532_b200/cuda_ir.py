@@ -161,6 +161,8 @@ class _Emit:
     def arr(self, ref) -> str:
         if ref.kind == "out":
             return "out"
+        if ref.kind == "workspace":
+            return f"W_{ref.tensor}"
         ti = self.order.index(ref.tensor)
         if ref.kind == "vals":
             return f"V{ti}"
@@ -265,7 +267,11 @@ class _Emit:
         elif isinstance(st, IR.AssertExtent):
             out.append(f"{pad}if ({self.e(st.actual)} != {self.e(st.expected)}) {{ atomicExch(err, 1); return; }}")  # noqa
         elif isinstance(st, IR.AllocWorkspace):
-            raise TypeError("workspaces are not emitted")
+            # precompute workspace (SPEC.md precompute): a thread-local array of
+            # the constant extent of the precomputed loop, zero-filled
+            if not isinstance(st.size, IR.IntLit):
+                raise TypeError("workspace extent must be a compile-time constant")
+            out.append(f"{pad}T W_{st.name}[{int(st.size.value)}] = {{}};")
         else:
             raise TypeError(f"cannot emit statement {st!r}")
 

@@ -282,6 +282,10 @@ class _TermLower:
         self.sym_of: dict[str, str] = {}
         self.loops: dict[str, tuple] = {}  # forest var -> (loop var, lo, hi)
         self.fmt = root.fmt
+        self.only = None  # precompute: the producer keeps only these accesses
+        self.exclude = []  # ... and the consumer drops them
+        self.extra = None  # ... and reads the workspace instead
+        self.track = root.track
         self._term_forest()
         self._choose_driver()
         self._plan_levels()
@@ -624,7 +628,7 @@ class _TermLower:
         hi = self.decl(f"{self.Dt}{k + 1}_shi", hi)
         name = self.fresh(f"{self.Dt}{k + 1}_p")
         deps = expr_refs(below) | expr_refs(lo) | expr_refs(hi)
-        if self.r.track:
+        if self.track:
             self.taken.add(name + "_s")
             init, step = track_recovery(arr, name, below, lo, hi)
             self.add(_Item("track", name, deps, [init, step],
@@ -671,6 +675,12 @@ class _TermLower:
         # every forest loop of this term exists (visit-exactly-once)
         for v in self.forest:
             self.r.loop_bounds(self, v)
+        # precompute split (program()): `only` keeps just these accesses (the
+        # producer of the workspace), `exclude` drops them and `extra` adds
+        # the workspace read (the consumer)
+        keep = (lambda a: a in self.only) if self.only is not None else (lambda a: a not in self.exclude)
+        if self.only is not None:
+            prod = None
         # driver
         if self.D is not None:
             n = len(self.D.vars)
@@ -679,9 +689,13 @@ class _TermLower:
                 self.P(k)
                 self.coord_at(k) if self.mode[k][0] != "locate" else None
             # every forest variable must reach the visited point: recover originals
-            prod = self.mul(prod, IR.Load(IR.ArrayRef("vals", self.Dt), pl))
+            if keep(self.D):
+                prod = self.mul(prod, IR.Load(IR.ArrayRef("vals", self.Dt), pl))
         for acc in self.others:
-            prod = self.mul(prod, self.access_value(acc))
+            if keep(acc):
+                prod = self.mul(prod, self.access_value(acc))
+        if self.extra is not None:
+            prod = self.mul(prod, self.extra)
         for v in self.stmt.assignment.all_vars:
             if v.name in self.used:
                 self.value(v.name)
@@ -787,14 +801,17 @@ class _Lowerer:
         return memo[key]
 
     # -- emission ---------------------------------------------------------------------
-    def lower_term(self, t: _TermLower, k_term: int):
+    def lower_term(self, t: _TermLower, k_term: int, store_to: str | None = None):
         IR = _ir()
         S = _S()
         idx, prod = t.build()
         race_tags = [self.stmt.tags_for(v) for v in t.forest]
         par = [(v, tg) for v, tg in zip(t.forest, race_tags) if tg.parallel_unit is not None]
         atomic_any = any(tg.race is S.RaceStrategy.ATOMICS for _, tg in par)
-        body_stmt = IR.ReduceAdd(IR.ArrayRef("out"), idx, prod, atomic=atomic_any)
+        if store_to is not None:  # precompute producer: workspace[innermost loop] = expr
+            body_stmt = IR.Store(IR.ArrayRef("workspace", store_to), _ref(self.loop_name(t, t.forest[-1])), prod)
+        else:
+            body_stmt = IR.ReduceAdd(IR.ArrayRef("out"), idx, prod, atomic=atomic_any)
         loops = [(v,) + tuple(self.loop_bounds(t, v)) for v in t.forest]
         for v, ln, _, _ in loops:
             self.loop_of[ln] = v
@@ -891,16 +908,139 @@ class _Lowerer:
                 out.append(s)
         return out
 
+    # -- precompute (SPEC.md §precompute: producer loop + workspace + consumer) -------
+    def _precompute_plan(self, t: "_TermLower", accs: list):
+        """(rec, matched accesses) when a precompute of this term can be
+        lowered as producer + workspace + consumer: its variable is the
+        term's innermost loop with a constant extent and its expression is a
+        sub-product of the term.  Otherwise None (lowered without the
+        workspace; the result is the same, SPEC.md precompute post)."""
+        from .generic import expand
+
+        IR = _ir()
+        for rec in self.stmt.precomputes:
+            if not t.forest or rec.var != t.forest[-1]:
+                continue
+            if not isinstance(self.loop_bounds(t, rec.var)[2], IR.IntLit):
+                continue
+            parts = expand(rec.expr)
+            if len(parts) != 1 or parts[0][0] != 1.0:
+                continue
+            pool = list(accs)
+            matched = []
+            for a in parts[0][1]:
+                if a not in pool:
+                    break
+                pool.remove(a)
+                matched.append(a)
+            else:
+                return rec, matched
+        return None
+
+    def _lower_precompute(self, t_c: "_TermLower", k: int, scal, accs, rec, matched):
+        import dataclasses
+
+        IR = _ir()
+        var = rec.var
+        ext = self.loop_bounds(t_c, var)[2]
+        t_c.exclude = matched
+        t_c.extra = IR.Load(IR.ArrayRef("workspace", rec.workspace), _ref(var))
+        consumer = self.lower_term(t_c, k)
+        # the producer: the same nest with only the precomputed factors, stored
+        # into the workspace; its innermost loop is renamed to the pre variable
+        t_p = _TermLower(self, 1.0, accs, k)
+        t_p.only = matched
+        t_p.track = False  # searches inside the (short, constant-extent) producer loop
+        saved = dict(self.loop_of)
+        producer = self.lower_term(t_p, k, store_to=rec.workspace)
+        self.loop_of = saved
+        loop = _find_loop(producer, var)
+        if loop is None:
+            return consumer
+        loop = _rename(loop, var, rec.pre_var)
+        tg = self.stmt.tags_for(rec.pre_var)
+        loop = dataclasses.replace(loop, parallel=None, unroll=tg.unroll or loop.unroll)
+        self.loop_of[rec.pre_var] = rec.pre_var
+        return _splice_before_loop(consumer, var, [IR.AllocWorkspace(rec.workspace, ext), loop])
+
     def program(self, dims: dict | None = None):
         IR = _ir()
         body: list = []
         for k, (scal, accs) in enumerate(self.terms):
             t = _TermLower(self, scal, accs, k)
-            stmts = self.lower_term(t, k)
+            pre = self._precompute_plan(t, accs)
+            if pre is None:
+                stmts = self.lower_term(t, k)
+            else:
+                stmts = self._lower_precompute(t, k, scal, accs, *pre)
             # each additive term is its own scope (its names are chosen per term)
             body.extend(stmts) if len(self.terms) == 1 else body.append(IR.Block(tuple(stmts)))
         manifest = _manifest(self.stmt, dims)
         return IR.Program(body=IR.Block(tuple(body)), manifest=manifest, name="compute")
+
+
+def _rename(node, old: str, new: str):
+    """Copy of an IR subtree with variable `old` renamed to `new`."""
+    import dataclasses
+
+    IR = _ir()
+    if isinstance(node, IR.VarRef):
+        return IR.VarRef(new) if node.name == old else node
+    if isinstance(node, IR.ForLoop) and node.var == old:
+        node = dataclasses.replace(node, var=new)
+    if dataclasses.is_dataclass(node) and not isinstance(node, type):
+        kw = {}
+        for f in dataclasses.fields(node):
+            v = getattr(node, f.name)
+            if isinstance(v, tuple):
+                kw[f.name] = tuple(_rename(x, old, new) for x in v)
+            elif dataclasses.is_dataclass(v) and not isinstance(v, type):
+                kw[f.name] = _rename(v, old, new)
+        return dataclasses.replace(node, **kw) if kw else node
+    return node
+
+
+def _splice_before_loop(stmts: list, var: str, pre: list):
+    """Insert `pre` right before the ForLoop over `var` (anywhere in the nest)."""
+    import dataclasses
+
+    IR = _ir()
+    out = []
+    for st in stmts:
+        if isinstance(st, IR.ForLoop) and st.var == var:
+            out.extend(pre)
+            out.append(st)
+        elif isinstance(st, IR.ForLoop):
+            out.append(dataclasses.replace(st, body=IR.Block(tuple(_splice_before_loop(list(st.body.stmts), var,
+                                                                                       pre)))))
+        elif isinstance(st, IR.If):
+            out.append(dataclasses.replace(st, then=IR.Block(tuple(_splice_before_loop(list(st.then.stmts), var,
+                                                                                       pre)))))
+        elif isinstance(st, IR.Block):
+            out.append(IR.Block(tuple(_splice_before_loop(list(st.stmts), var, pre))))
+        else:
+            out.append(st)
+    return out
+
+
+def _find_loop(stmts, var: str):
+    IR = _ir()
+    for st in stmts:
+        if isinstance(st, IR.ForLoop):
+            if st.var == var:
+                return st
+            r = _find_loop(st.body.stmts, var)
+            if r is not None:
+                return r
+        elif isinstance(st, IR.If):
+            r = _find_loop(st.then.stmts, var)
+            if r is not None:
+                return r
+        elif isinstance(st, IR.Block):
+            r = _find_loop(st.stmts, var)
+            if r is not None:
+                return r
+    return None
 
 
 def _manifest(stmt, dims):

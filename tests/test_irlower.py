@@ -265,3 +265,14 @@ def test_random_schedules_on_corpus_expressions(k):
         done += 1
         err = np.max(np.abs(got - want) / np.maximum(1.0, np.abs(want))) if want.size else 0.0
         assert err <= 1e-10, (expr, steps, err)
+
+
+def test_precompute_lowers_to_producer_workspace_consumer():
+    """SPEC.md precompute: AllocWorkspace + producer loop over the pre
+    variable (with its unroll tag) + consumer loop reading the workspace."""
+    prog = lower_ir(corpus.build("A2"), {"A": (40, 50), "x": (50,)})
+    text = IR.format_program(prog)
+    assert "workspace precomputed[8]: f64 = 0" in text
+    assert "for thread_nz_pre in [0, 8) unroll(8)" in text
+    assert "precomputed[thread_nz_pre] = (A_vals[fpos] * x_vals[j])" in text
+    assert "out[i] += atomic precomputed[thread_nz]" in text
