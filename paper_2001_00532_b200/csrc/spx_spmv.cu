@@ -350,9 +350,6 @@ __global__ void __launch_bounds__(kMaxThreads, 2) spmv_nnz_kernel(const int32_t*
 // CTA barrier and no carry fix-up.  fp64 sums of a row split across warps
 // may differ in the last bits from run to run (atomic order).
 constexpr int kWarpPos = 320;  // pos entries staged per warp
-#ifndef SPX_SPMV_HIST
-#define SPX_SPMV_HIST 1  // rows of the 32 lanes from a histogram + scan (else a binary search per lane)
-#endif
 #ifndef SPX_SPMV_CARVEOUT
 #define SPX_SPMV_CARVEOUT 20  // percent of 228 KB: 4 CTAs x 8 warps x 1.25 KB of pos slices fit the 64 KB config
 #endif
@@ -403,56 +400,18 @@ __global__ void __launch_bounds__(kMaxThreads, SPX_SPMV_MINB) spmv_nnz_atomic_ke
   const int rlo = __ldg(first + q), rhi = __ldg(first + q + 1);
   const int nstage = rhi - rlo + 2;  // pos[rlo .. rhi+1]
   const bool staged = nstage <= kWarpPos;
-#if SPX_SPMV_HIST
-  // SearchSegment (ir.py:178-190) for all 32 lanes at once: row boundary k
-  // (pos[rlo+k], k >= 1) is at or before lane t's start a_t = q0 + t*tpt
-  // for every t >= c_k = ceil((pos[rlo+k] - q0) / tpt); a per-warp histogram
-  // of c_k and a lane scan give each lane its row without a dependent chain
-  // of shared-memory reads
-  int32_t* s_cnt = s_pos + kWarpPos - 32;  // the slice's last 32 slots (staging stops short of them)
-  const bool hist = staged && nstage <= kWarpPos - 32 && TPT > 0;
-  if (hist) s_cnt[lane] = 0;
-  __syncwarp();  // the counters are zero before any lane adds to them
-  if (staged)
-    for (int k = lane; k < nstage; k += 32) {
-      const int pk = __ldg(pos + rlo + k);
-      s_pos[k] = pk;
-      if (hist && k >= 1 && k < nstage - 1) {
-        const int c = (pk - q0 + tpt - 1) / tpt;  // pk >= q0 for k >= 1
-        if (c < 32) atomicAdd(s_cnt + c, 1);
-      }
-    }
-  __syncwarp();
-#else
-  const bool hist = false;
   if (staged)
     for (int k = lane; k < nstage; k += 32) s_pos[k] = __ldg(pos + rlo + k);
   __syncwarp();
-#endif
 #define SPX_P(r) (staged ? s_pos[(r) - rlo] : __ldg(pos + (r)))
-  int rows_before = 0;
-#if SPX_SPMV_HIST
-  if (hist) {
-    rows_before = s_cnt[lane];
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(kFull, rows_before, o);
-      if (lane >= o) rows_before += y;
-    }
-  }
-#endif
   int32_t head = -1;
   T hval = T(0);
   if (n > 0) {
     int lo = rlo, hi = rhi + 1;  // SearchSegment (ir.py:178-190)
-    if (hist) {
-      lo = rlo + rows_before + 1;
-    } else {
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (SPX_P(mid) <= a) lo = mid + 1;
-        else hi = mid;
-      }
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (SPX_P(mid) <= a) lo = mid + 1;
+      else hi = mid;
     }
     int r = lo - 1;
     bool is_head = SPX_P(r) < a;
