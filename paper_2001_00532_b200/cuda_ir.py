@@ -77,7 +77,6 @@ class _Emit:
         self.guard_tags: list = []
         self.mapping: dict = {}
         self.inst: dict = {}
-        self.n_cnt = 0
         self._plan_units()
 
     # -- parallel units ------------------------------------------------------------
