@@ -164,23 +164,11 @@ def _dims_of(x) -> tuple:
 
 
 def _check_extents(program: Program, inputs: dict) -> dict:
-    """tensors.py:271-289 semantics (DimensionMismatchError on conflict)."""
-    E = _spindle.errors
-    extents: dict[str, int] = {}
-    dims = {}
-    for acc in program.stmt.assignment.input_accesses():
-        if acc.tensor not in inputs:
-            raise E.TensorError(f"tensor {acc.tensor!r} is not bound")
-        d = _dims_of(inputs[acc.tensor])
-        dims[acc.tensor] = d
-        if len(d) != len(acc.vars):
-            raise E.DimensionMismatchError(
-                f"access {acc!r} has {len(acc.vars)} variables but tensor has order {len(d)}")
-        for v, n in zip(acc.vars, d):
-            if v.name in extents and extents[v.name] != n:
-                raise E.DimensionMismatchError(f"variable {v.name!r} used with extents {extents[v.name]} and {n}")
-            extents.setdefault(v.name, int(n))
-    return dims
+    """Extent checks by the reference's own `variable_extents` (tensors.py:271-289:
+    TensorError for an unbound tensor, DimensionMismatchError on an order or
+    extent conflict); returns each input's dims."""
+    _spindle.tensors.variable_extents(program.stmt.assignment, inputs)
+    return {acc.tensor: _dims_of(inputs[acc.tensor]) for acc in program.stmt.assignment.input_accesses()}
 
 
 def _check_formats(program: Program, ops: dict) -> None:
