@@ -63,7 +63,7 @@ def parse():
     ap.add_argument("--ncols", type=int, default=128)
     ap.add_argument("--tb", type=int, default=4096, help="NNZ_PER_TB")
     ap.add_argument("--warp", type=int, default=512, help="NNZ_PER_WARP")
-    ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--e2e-steps", type=int, default=16)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--no-secondary", action="store_true", help="skip the cfg5 SpMV / cfg4 MTTKRP records")
@@ -294,6 +294,52 @@ class Timer:
         if world > 1:
             dist.barrier()
         return [s.elapsed_time(e) for s, e in zip(self.starts, self.ends)]
+
+
+def link_bound(torch, dev, h2d: int, d2h: int, upload_streams: int = 2) -> dict:
+    """Pinned host<->device rates on this box, measured here: H2D split over
+    `upload_streams` streams (the Pipeline's layout), D2H alone, and both at
+    once (PCIe is full duplex but the two directions share it).  `bound_ms`
+    is the time the step's copies need at those rates: the overlapped phase
+    runs both directions at the duplex rate until the smaller one is done,
+    the rest of the larger one runs alone."""
+    n = 256 << 20
+    h = torch.empty(n, dtype=torch.uint8).pin_memory()
+    h2 = torch.empty(n, dtype=torch.uint8).pin_memory()
+    d = torch.empty(n, dtype=torch.uint8, device=dev)
+    d2 = torch.empty(n, dtype=torch.uint8, device=dev)
+    ups = [torch.cuda.Stream(dev) for _ in range(upload_streams)]
+    down = torch.cuda.Stream(dev)
+    part = n // upload_streams
+
+    def up():
+        for k, st in enumerate(ups):
+            with torch.cuda.stream(st):
+                d[k * part:(k + 1) * part].copy_(h[k * part:(k + 1) * part], non_blocking=True)
+
+    def dn():
+        with torch.cuda.stream(down):
+            h2.copy_(d2, non_blocking=True)
+
+    def rate(fns, nbytes, reps=4):
+        for f in fns:
+            f()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            for f in fns:
+                f()
+        torch.cuda.synchronize(dev)
+        return nbytes * reps / (time.perf_counter() - t0)
+
+    r_up, r_dn = rate([up], n), rate([dn], n)
+    r_both = rate([up, dn], 2 * n) / 2  # per direction while both run
+    lo = min(h2d, d2h)
+    rest = (h2d - lo) / r_up if h2d > d2h else (d2h - lo) / r_dn
+    bound = lo / r_both + rest
+    del h, h2, d, d2
+    return {"h2d_GBs": round(r_up / 1e9, 2), "d2h_GBs": round(r_dn / 1e9, 2),
+            "duplex_GBs_per_direction": round(r_both / 1e9, 2), "bound_ms": round(bound * 1e3, 3)}
 
 
 def max_over_ranks(torch, dist, world, vals, dev, shared):
@@ -648,6 +694,10 @@ def main():
                       + (", max over ranks" if world > 1 else "")
                       + (", B uploaded as 1/N row shares + NCCL all-gather (spx_gather)" if comm is not None else ""),
                "sync_interpret": {"value": round(flops / sync_t / 1e9, 3), "ms_per_step": round(sync_t * 1e3, 3)}}
+        # the copies' own floor on this box's PCIe link (per rank: its bytes)
+        link = link_bound(torch, dev, pipe.h2d_bytes, pipe.d2h_bytes)
+        link["frac"] = round(link["bound_ms"] / (e_t * 1e3), 3)
+        e2e["link"] = link
         ref = torch.empty_like(hout)
         interpret(prog, {"A": hA, "B": hB}, out=ref)
         assert torch.equal(hout.view(-1), ref.view(-1)), "pipelined e2e result differs from interpret"
