@@ -549,12 +549,12 @@ __device__ __forceinline__ void mttkrp_walk(const MttkrpCtx<T, VPL, CONTIG>& c, 
 #define SPX_MTTKRP_QUARTER 1
 #endif
 #ifndef SPX_MQ_RING
-#define SPX_MQ_RING 2
+#define SPX_MQ_RING 3  // batch bi in use, bi+1 landed (its D rows prefetched), bi+2 in flight
 #endif
 #ifndef SPX_MQ_CARVEOUT
 #define SPX_MQ_CARVEOUT 14  // percent of 228 KB: the 32 KB shared-memory config, L1 keeps 224 KB for D
 #endif
-constexpr int kQRing = SPX_MQ_RING;       // slots of 8 leaves per quarter in flight
+constexpr int kQRing = SPX_MQ_RING;       // slots of QB leaves per quarter in flight
 #ifndef SPX_MQ_THREADS
 #define SPX_MQ_THREADS 512  // x 2 CTAs/SM (same-box A/B: 24 warps at 80 registers ran slower than 32 at 64)
 #endif
@@ -565,6 +565,10 @@ constexpr int kQThreads = SPX_MQ_THREADS;
 #ifndef SPX_MQ_SMWIN
 #define SPX_MQ_SMWIN 1  // fiber window in shared memory (else per-lane registers + width-8 shuffles)
 #endif
+#ifndef SPX_MQ_PF
+#define SPX_MQ_PF 1  // prefetch the next batch's D rows into L1 (needs SPX_MQ_RING >= 3): cfg4 1.013 vs 1.038 ms
+#endif
+static_assert(!SPX_MQ_PF || SPX_MQ_RING >= 3, "the next-batch prefetch needs a 3-slot ring");
 #ifndef SPX_MQ_QB
 #define SPX_MQ_QB 16  // leaves per quarter per batch with 16 B copies (8: half the lanes copy)
 #endif
@@ -750,10 +754,28 @@ __global__ void __launch_bounds__(kQThreads, SPX_MQ_MINB) mttkrp_quarter_kernel(
     for (int bi = 0; bi < nbw; ++bi) {
       issue(bi + kQRing - 1, islot);
       islot = islot == (kQRing - 1) * kSlot ? 0 : islot + kSlot;
+#if SPX_MQ_PF
+      // batch bi+1 has landed too: pull its D rows into L1 while batch bi is
+      // processed (each lane of the quarter prefetches QB/8 of its rows)
+      cp_async_wait<kQRing - 2>();
+      __syncwarp();
+      const uint32_t sl = ring_s + rslot + rd_off;
+      rslot = rslot == (kQRing - 1) * kSlot ? 0 : rslot + kSlot;
+      if (bi + 1 < nbw) {
+        const uint32_t sn = ring_s + rslot + rd_off + ql * (QB / 2);
+#pragma unroll
+        for (int j = 0; j < QB / 8; ++j) {
+          int lj;
+          asm volatile("ld.shared.s32 %0, [%1];" : "=r"(lj) : "r"(sn + 4 * j));
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(addr_wide(Dl, (uint32_t)lj, rowb)));
+        }
+      }
+#else
       cp_async_wait<kQRing - 1>();
       __syncwarp();
       const uint32_t sl = ring_s + rslot + rd_off;
       rslot = rslot == (kQRing - 1) * kSlot ? 0 : rslot + kSlot;
+#endif
 #pragma unroll
       for (int h = 0; h < QB / 4; ++h, pp += 4) {
         const int4 l4 = lds_i4(sl + h * 16);
