@@ -615,6 +615,16 @@ def main():
             # this part (18.9 TB/s: L2-resident rows, no arithmetic; tools/gbench2.py,
             # profiles/r01_gather_paths.txt)
             "gather_frac": round(nnz_local * N * 4 / (statistics.mean(times) * 1e-3) / 18.9e12, 3)}
+    # the binding limit: every byte of B enters an SM through its L2->SM
+    # crossbar port, 64 B/clk/SM (ncu l1tex__m_xbar2l1tex_read_bytes,
+    # profiles/r02_spmm_ceiling.txt), at the SM clock sampled in the timed region
+    sm_mhz = (clocks or {}).get("sm_mhz")
+    if sm_mhz:
+        n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+        port = 64.0 * n_sm * sm_mhz * 1e6
+        roof["port_bound"] = {"bytes_per_clk_per_sm": 64, "sms": n_sm, "sm_mhz": sm_mhz,
+                              "TBs": round(port / 1e12, 2),
+                              "frac": round(nnz_local * N * 4 / (statistics.mean(times) * 1e-3) / port, 3)}
     if world > 1:
         roof["frac_aggregate"] = round(sum_over_ranks(torch, dist, world, [cb_local], dev, shared)[0]
                                        / (world * hbm * 1e9 * t_ms * 1e-3), 4)

@@ -81,6 +81,9 @@ extern "C" {
  *  7   TTV fiber-split           A(i,j)=B(i,j,k)*c(k) B:sss   [0]=FIBERS_PER_TB [1]=FIBERS_PER_WARP
  *  8   MTTKRP nnz-split          A(i,j)=B(i,k,l)*C(k,j)*D(l,j) [0]=NNZ_PER_TB [1]=NNZ_PER_WARP [2]=WARP_SIZE [3]=bound
  *  9   MTTKRP slice-split        "                        [0]=SLICES_PER_TB [1]=WARPS_PER_TB
+ *                                                         [2]=1: cut slices heavier than max(4096, nnz/8192) leaves into
+ *                                                         leaf ranges, partial rows folded in range order (workspace);
+ *                                                         0: one warp per slice (a GPU schedule's warp-per-slice)
  *  10  SDDMM row-split           A(i,j)=B(i,j)*C(i,k)*D(j,k)  [0]=ROWS_PER_TB [1]=WARPS_PER_TB [2]=WARP_SIZE [3]=bound [7]=dense_out
  *  11  TTV nnz-split             A(i,j)=B(i,j,k)*c(k) B:sss   [0]=NNZ_PER_TB [1]=NNZ_PER_WARP [2]=NNZ_PER_THREAD
  *

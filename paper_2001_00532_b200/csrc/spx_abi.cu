@@ -182,6 +182,7 @@ size_t spx_workspace_size(const spx_plan* plan, const int32_t* dims) {
     case SPX_K_SPMV_NNZ: return ws_spmv(plan->kernel_id, a);
     case SPX_K_SPMM_NNZ: return ws_spmm(plan->kernel_id, a);
     case SPX_K_MTTKRP_NNZ:
+    case SPX_K_MTTKRP_SLICE:
     case SPX_K_TTV_NNZ: return ws_csf(plan->kernel_id, a);
     case SPX_K_SDDMM_NNZ: return ws_sddmm(plan->kernel_id, a);
     default: return 0;

@@ -286,7 +286,7 @@ struct MttkrpCtx {
 // runs segment by segment with the products masked (FSEL) to the segment.
 template <bool OWNED, int G>
 __device__ __forceinline__ void mttkrp_walk_quad(const MttkrpCtx<float, 1, true>& c, unsigned char* ring_base,
-                                                 int lane, int q0, int q1, int f, int s) {
+                                                 int lane, int q0, int q1, int f, int s, float* part_dst) {
   static_assert(G == 4 || G == 8, "whole 16 B vectors of coordinates / values per quarter");
   // fiber window: ends and k coordinates of fibers [fb, fb+32), per warp in
   // shared memory (broadcast reads, no shuffles in the divergent close path)
@@ -326,7 +326,7 @@ __device__ __forceinline__ void mttkrp_walk_quad(const MttkrpCtx<float, 1, true>
       x.w += __shfl_xor_sync(kFull, x.w, o);
     }
     if (qw == 0) {
-      float4* dst = reinterpret_cast<float4*>(c.A + (int64_t)__ldg(c.crd0 + s) * 32) + ql;
+      float4* dst = reinterpret_cast<float4*>(part_dst ? part_dst : c.A + (int64_t)__ldg(c.crd0 + s) * 32) + ql;
       if constexpr (OWNED) *dst = x;
       else atomicAdd(dst, x);
     }
@@ -409,14 +409,18 @@ __device__ __forceinline__ void mttkrp_walk_quad(const MttkrpCtx<float, 1, true>
 
 // Walk leaves [q0, q1); f = fiber holding q0, s = slice holding f.
 // OWNED: the warp owns every slice it touches completely (plain stores).
-template <typename T, int VPL, bool CONTIG, bool OWNED>
+// part_dst (OWNED, a range inside one slice): the slice partial goes there
+// instead of A's row (a part of a split slice, folded by slice_fold_kernel).
+// QG: leaves per quarter per group of the rank-32 walk (0 = the default:
+// SPX_MTTKRP_SLICE_G for OWNED, whose whole-slice warps are latency-bound
+// at 1 CTA/SM, SPX_MTTKRP_G otherwise).
+template <typename T, int VPL, bool CONTIG, bool OWNED, int QG = 0>
 __device__ __forceinline__ void mttkrp_walk(const MttkrpCtx<T, VPL, CONTIG>& c, unsigned char* ring_base, int lane,
-                                            int q0, int q1, int f, int s) {
+                                            int q0, int q1, int f, int s, T* part_dst = nullptr) {
   if constexpr (std::is_same<T, float>::value && VPL == 1 && CONTIG) {
     if (c.R == 32) {
-      // slice-split (OWNED): one warp walks a whole slice, so the largest slice is
-      // latency-bound and gets twice the leaves in flight (the kernel runs 1 CTA/SM)
-      mttkrp_walk_quad<OWNED, OWNED ? SPX_MTTKRP_SLICE_G : SPX_MTTKRP_G>(c, ring_base, lane, q0, q1, f, s);
+      constexpr int G = QG ? QG : (OWNED ? SPX_MTTKRP_SLICE_G : SPX_MTTKRP_G);
+      mttkrp_walk_quad<OWNED, G>(c, ring_base, lane, q0, q1, f, s, part_dst);
       return;
     }
   }
@@ -444,7 +448,7 @@ __device__ __forceinline__ void mttkrp_walk(const MttkrpCtx<T, VPL, CONTIG>& c, 
   accs.zero();
   crow.load(c.Cm + fiber_k(f) * Ri, lane, ncols);
   auto flush_slice = [&]() {
-    T* dst = c.A + (int64_t)__ldg(c.crd0 + s) * c.R;
+    T* dst = part_dst ? part_dst : c.A + (int64_t)__ldg(c.crd0 + s) * c.R;
     if constexpr (OWNED) accs.store(dst, lane, ncols);
     else accs.atomic_add_into(dst, lane, ncols);
     accs.zero();
@@ -862,22 +866,110 @@ __global__ void __launch_bounds__(kMttkrpThreads, SPX_MTTKRP_MINB) mttkrp_nnz_ke
   }
 }
 
-// K9: slice-split (A.5 shape) -- one warp per slice, plain stores;
-// persistent CTAs walk the slices round-robin.
-template <typename T, int VPL, bool CONTIG>
-__global__ void __launch_bounds__(kMttkrpThreads, SPX_MTTKRP_SLICE_MINB) mttkrp_slice_kernel(
+// K9: slice-split (A.5 shape) -- every slice has one owner and no output
+// races.  A slice of at most `part` leaves is one unit: one warp walks it and
+// stores A's row.  A heavier slice is cut into ceil(leaves / part) leaf
+// ranges; their warps store partial rows into the workspace and
+// slice_fold_kernel adds them in range order (deterministic, no atomics).
+// Without the cut the heaviest slice sets the time: at cfg4 (2,048 slices,
+// the largest 890K leaves) one warp per slice ran 15.9 ms.
+// unit -> (slice, range): part_start[s] = first unit of slice s (scan of
+// max(1, ceil(leaves_s / part)) by slice_parts_kernel), part_start[S] = units.
+__global__ void slice_parts_kernel(const int32_t* __restrict__ pos1, const int32_t* __restrict__ pos2, int64_t S,
+                                   int64_t part, int32_t* __restrict__ part_start) {
+  __shared__ int64_t s_warp[32];
+  __shared__ int64_t s_base;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  if (tid == 0) s_base = 0;
+  __syncthreads();
+  for (int64_t t0 = 0; t0 < S; t0 += blockDim.x) {
+    const int64_t s = t0 + tid;
+    int64_t np = 0;
+    if (s < S) {
+      const int64_t leaves = (int64_t)__ldg(pos2 + __ldg(pos1 + s + 1)) - __ldg(pos2 + __ldg(pos1 + s));
+      np = leaves > part ? (leaves + part - 1) / part : 1;
+    }
+    int64_t x = np;  // inclusive warp scan
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      int64_t w = lane < nw ? s_warp[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t y = __shfl_up_sync(kFull, w, o);
+        if (lane >= o) w += y;
+      }
+      if (lane < nw) s_warp[lane] = w;  // inclusive over warps
+    }
+    __syncthreads();
+    const int64_t base = s_base;
+    if (s < S) part_start[s] = (int32_t)(base + (warp ? s_warp[warp - 1] : 0) + x - np);
+    __syncthreads();
+    if (tid == 0) s_base = base + s_warp[nw - 1];
+    __syncthreads();
+  }
+  if (tid == 0) part_start[S] = (int32_t)s_base;
+}
+
+// SPLIT (params[2] = 1): balanced units, 2 CTAs/SM and the nnz-split's group
+// depth (cfg4 MTTKRP0: 1.42 ms, against 2.04 at 1 CTA/SM with G = 8);
+// whole-slice warps keep 1 CTA/SM and G = 8 for the latency-bound heaviest slice.
+template <typename T, int VPL, bool CONTIG, bool SPLIT>
+__global__ void __launch_bounds__(kMttkrpThreads, SPLIT ? SPX_MTTKRP_MINB : SPX_MTTKRP_SLICE_MINB) mttkrp_slice_kernel(
     const int32_t* __restrict__ crd0, const int32_t* __restrict__ pos1, const int32_t* __restrict__ crd1,
     const int32_t* __restrict__ pos2, const int32_t* __restrict__ crd2, const T* __restrict__ vals,
-    const T* __restrict__ Cm, const T* __restrict__ Dm, T* __restrict__ A, int64_t S, int64_t F, int64_t R) {
+    const T* __restrict__ Cm, const T* __restrict__ Dm, T* __restrict__ A, int64_t S, int64_t F, int64_t R,
+    const int32_t* __restrict__ part_start, int64_t part, T* __restrict__ partial) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* ring = smem_raw + (size_t)warp * LeafRing<T, kLeafRing>::kBytes;
   MttkrpCtx<T, VPL, CONTIG> c{crd0, pos1, crd1, pos2, crd2, vals, Cm, Dm, A, S, F, R};
-  for (int64_t s = (int64_t)blockIdx.x * nw + warp; s < S; s += (int64_t)gridDim.x * nw) {
+  const int64_t units = __ldg(part_start + S);
+  for (int64_t u = (int64_t)blockIdx.x * nw + warp; u < units; u += (int64_t)gridDim.x * nw) {
+    const int64_t s = warp_search_segment(part_start, 0, S, u, lane);
+    const int64_t k = u - __ldg(part_start + s), np = __ldg(part_start + s + 1) - __ldg(part_start + s);
     const int f0 = __ldg(pos1 + s), f1 = __ldg(pos1 + s + 1);
     const int q0 = __ldg(pos2 + f0), q1 = __ldg(pos2 + f1);
-    if (q0 < q1) mttkrp_walk<T, VPL, CONTIG, true>(c, ring, lane, q0, q1, f0, (int)s);
+    constexpr int QG = SPLIT ? SPX_MTTKRP_G : SPX_MTTKRP_SLICE_G;
+    if (np == 1) {
+      if (q0 < q1) mttkrp_walk<T, VPL, CONTIG, true, QG>(c, ring, lane, q0, q1, f0, (int)s);
+    } else {
+      const int a = (int)(q0 + k * part), b = (int)min((int64_t)q1, (int64_t)a + part);
+      const int f = (int)warp_search_segment(pos2, f0, f1, a, lane);  // fiber holding leaf a
+      mttkrp_walk<T, VPL, CONTIG, true, QG>(c, ring, lane, a, b, f, (int)s, partial + u * R);
+    }
   }
+}
+
+// A[crd0[s], :] = sum of slice s's partial rows in range order (split slices only)
+template <typename T>
+__global__ void slice_fold_kernel(const int32_t* __restrict__ part_start, const int32_t* __restrict__ crd0,
+                                  int64_t S, int64_t R, const T* __restrict__ partial, T* __restrict__ A) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t s = g >> 5;
+  if (s >= S) return;
+  const int u0 = __ldg(part_start + s), u1 = __ldg(part_start + s + 1);
+  if (u1 - u0 < 2) return;
+  T* dst = A + (int64_t)__ldg(crd0 + s) * R;
+  for (int64_t j = g & 31; j < R; j += 32) {
+    T acc = partial[(int64_t)u0 * R + j];
+    for (int u = u0 + 1; u < u1; ++u) acc += partial[(int64_t)u * R + j];
+    dst[j] = acc;
+  }
+}
+
+// leaves per K9 unit: slices heavier than this are cut (about 8,192 units at
+// scale, so the largest unit is a small share of a warp's work)
+#ifndef SPX_SLICE_UNITS
+#define SPX_SLICE_UNITS 8192
+#endif
+inline int64_t slice_part_leaves(int64_t nnz) {
+  return std::max<int64_t>(4096, (nnz + SPX_SLICE_UNITS - 1) / SPX_SLICE_UNITS);
 }
 
 int num_sms() {
@@ -1026,11 +1118,30 @@ int run_mttkrp(int kid, const Args& a) {
     count_launch();
     return check_cuda(cudaGetLastError(), "mttkrp_nnz_kernel");
   }
-  auto kern = mttkrp_slice_kernel<T, VPL, CONTIG>;
-  kern<<<(unsigned)grid_for(kern, c.S), kMttkrpThreads, smem, a.stream>>>(c.crd0, c.pos1, c.crd1, c.pos2, c.crd2,
-                                                                         vals, Cm, Dm, A, c.S, c.F, R);
+  // K9: units of whole slices or leaf ranges of split slices (slice_parts_kernel);
+  // params[2] == 0 (a GPU schedule's warp per slice): no slice is split
+  const int64_t part = a.params[2] ? slice_part_leaves(c.nnz) : (int64_t)INT32_MAX;
+  const int64_t max_units = c.S + (a.params[2] ? ceil_div(c.nnz, part) : 0);
+  const size_t ps_bytes = (size_t)ceil_div((c.S + 1) * (int64_t)sizeof(int32_t), 256) * 256;
+  const size_t need = ps_bytes + (size_t)max_units * (size_t)R * sizeof(T);
+  if (!a.ws || a.ws_bytes < need) return fail(SPX_E_WORKSPACE, "workspace %zu < %zu bytes", a.ws_bytes, need);
+  int32_t* part_start = static_cast<int32_t*>(a.ws);
+  T* partial = reinterpret_cast<T*>(static_cast<char*>(a.ws) + ps_bytes);
+  slice_parts_kernel<<<1, 1024, 0, a.stream>>>(c.pos1, c.pos2, c.S, part, part_start);
   count_launch();
-  return check_cuda(cudaGetLastError(), "mttkrp_slice_kernel");
+  if (int e = check_cuda(cudaGetLastError(), "slice_parts_kernel")) return e;
+  auto kern = a.params[2] ? mttkrp_slice_kernel<T, VPL, CONTIG, true> : mttkrp_slice_kernel<T, VPL, CONTIG, false>;
+  kern<<<(unsigned)grid_for(kern, max_units), kMttkrpThreads, smem, a.stream>>>(
+      c.crd0, c.pos1, c.crd1, c.pos2, c.crd2, vals, Cm, Dm, A, c.S, c.F, R, part_start, part, partial);
+  count_launch();
+  if (int e = check_cuda(cudaGetLastError(), "mttkrp_slice_kernel")) return e;
+  if (max_units > c.S) {  // some slice may be split
+    slice_fold_kernel<T><<<(unsigned)ceil_div(c.S * 32, 256), 256, 0, a.stream>>>(part_start, c.crd0, c.S, R,
+                                                                                    partial, A);
+    count_launch();
+    if (int e = check_cuda(cudaGetLastError(), "slice_fold_kernel")) return e;
+  }
+  return SPX_OK;
 }
 
 template <typename T>
@@ -1419,6 +1530,13 @@ size_t ws_csf(int kid, const Args& a) {
     if (tpt == 4 || tpt == 8 || tpt == 16)  // the streaming form: the chunk table (fiber, slice)
       return (size_t)2 * (size_t)ceil_div(a.level_sizes[2] > 0 ? a.level_sizes[2] : 1, 32 * tpt) * sizeof(int32_t);
     return ttv_nnz_layout(a).total;
+  }
+  if (kid == SPX_K_MTTKRP_SLICE) {  // unit table + partial rows of split slices
+    const int64_t S = a.level_sizes[0], nnz = a.level_sizes[2], R = a.dims[1][1];
+    if (nnz <= 0) return 0;
+    const size_t es = a.dtype == SPX_F32 ? 4 : 8;
+    const int64_t units = S + (a.params[2] ? ceil_div(nnz, slice_part_leaves(nnz)) : 0);
+    return (size_t)ceil_div((S + 1) * 4, 256) * 256 + (size_t)units * (size_t)R * es;
   }
   if (kid != SPX_K_MTTKRP_NNZ) return 0;
   const int64_t nnz = a.level_sizes[2];

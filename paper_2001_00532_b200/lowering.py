@@ -414,6 +414,12 @@ def _check_tags(sh: _Shape, kernel_vars: dict, kernel: str) -> None:
             )
 
 
+def _gpu_tagged(sh: _Shape) -> bool:
+    """Does the schedule place any loop on a GPU unit?  CPU-tagged and
+    unscheduled statements leave the GPU mapping to the kernel."""
+    return any((t := sh.stmt.tags_for(n).parallel_unit) is not None and t.value in _GPU_UNITS for n in sh.forest)
+
+
 # ---------------------------------------------------------------------------
 # per-class tables
 # ---------------------------------------------------------------------------
@@ -535,7 +541,12 @@ def _match_mttkrp(sh: _Shape) -> Program:
         if div:
             raise _NoMatch
         kv = {"block": rows.get("block"), "warp": rows.get("warp", rows.get("row"))}
-        return Program(sh.stmt, ec, _lib.K_MTTKRP_SLICE, [R or 8, Wn or min(R or 8, 8)], vars=kv)
+        # params[2] = 1: heavy slices are cut into leaf ranges whose partial
+        # rows are folded in order (still one owner per output row, no
+        # atomics) -- only when no GPU unit is named; a GPU schedule's
+        # warp-per-slice (K9) runs as written, imbalance included
+        return Program(sh.stmt, ec, _lib.K_MTTKRP_SLICE,
+                       [R or 8, Wn or min(R or 8, 8), 0 if _gpu_tagged(sh) else 1], vars=kv)
     raise _NoMatch
 
 

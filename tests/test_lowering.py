@@ -168,3 +168,13 @@ def test_unlaunchable_constants_do_not_select_a_table_kernel(entry, params):
 def test_launchable_constants_still_select_the_table():
     assert lower(corpus.build("A4", NNZ_PER_TB=512 * 16, NNZ_PER_WARP=512)).kernel == "spmm_nnz"
     assert lower(corpus.build("A2", NNZ_PER_TB=512 * 4, NNZ_PER_WARP=128, NNZ_PER_THREAD=4)).kernel == "spmv_nnz"
+
+
+def test_slice_split_cut_only_without_gpu_units():
+    """K9's heavy-slice cut (params[2]) is for CPU-tagged / unscheduled
+    MTTKRP; a GPU schedule's warp-per-slice runs as written."""
+    from paper_2001_00532_b200 import corpus, lower
+
+    assert lower(corpus.build("A5", CHUNK_SIZE=8)).params[2] == 1
+    assert lower(corpus.build("MTTKRP0")).params[2] == 1
+    assert lower(corpus.build("K9", SLICES_PER_TB=8)).params[2] == 0
