@@ -49,7 +49,7 @@ CORPUS = [
     Entry("A1", "PAPER.md:1890-1900 SpMV CPU", SPMV, F_SPMV,
           """split(i, i0, i1, {CHUNK_SIZE})
 reorder(i0, i1, j)
-parallelize(i0, CPUThread, NoRaces)""", {"CHUNK_SIZE": 16}, "spmv_row"),
+parallelize(i0, CPUThread, NoRaces)""", {"CHUNK_SIZE": 16}, "spmv_warp"),
     Entry("A2", "PAPER.md:1902-1925 SpMV GPU", SPMV_PRE, F_SPMV,
           """fuse(i, j, f)
 pos(f, fpos, A(i,j))
@@ -183,7 +183,7 @@ parallelize(block, GPUBlock, NoRaces)
 parallelize(warp, GPUWarp, NoRaces)""", {"SLICES_PER_TB": 8}, "mttkrp_slice"),
     Entry("K10", "row-split SDDMM (unscheduled SDDMM shape)", SDDMM, F_SDDMM, "", {}, "sddmm_row"),
     Entry("TTV0", "unscheduled TTV", TTV, F_TTV, "", {}, "ttv_fiber"),
-    Entry("SPMV0", "unscheduled SpMV (Fig. 2b)", SPMV, F_SPMV, "", {}, "spmv_row"),
+    Entry("SPMV0", "unscheduled SpMV (Fig. 2b)", SPMV, F_SPMV, "", {}, "spmv_warp"),
     Entry("MTTKRP0", "unscheduled MTTKRP", MTTKRP, F_MTTKRP, "", {}, "mttkrp_slice"),
 ]
 

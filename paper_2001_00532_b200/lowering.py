@@ -459,7 +459,15 @@ def _match_spmv(sh: _Shape) -> Program:
         return Program(sh.stmt, ec, _lib.K_SPMV_WARP, [R or 8, Wn or min(R or 8, 8)], row_divide=div, vars=kv)
     if len(jg) != 1 or next(iter(jg.values())).path != ():
         raise _NoMatch
-    # K1 thread-per-row (A.7, A.1, unscheduled)
+    if not _gpu_tagged(sh):
+        # A.1 (CPU tags) and the unscheduled loop nest (Fig. 2b) name no GPU
+        # unit: each row keeps one owner, but the owner is a warp (K2, lanes
+        # over the row's positions, a fixed shuffle fold) rather than a thread
+        # -- cfg5: 1.73 ms against 9.2 ms thread per row
+        R = rp[0] or 8
+        kv = {"block": rows.get("block"), "warp": rows.get("row", rows.get("warp"))}
+        return Program(sh.stmt, ec, _lib.K_SPMV_WARP, [R, min(R, 8)], row_divide=div, vars=kv)
+    # K1 thread-per-row (A.7: the GPU schedule's thread per row, imbalance included)
     kv = {"block": rows.get("block"), "thread": rows.get("row", rows.get("warp"))}
     return Program(sh.stmt, ec, _lib.K_SPMV_ROW, [rp[0] or 256], row_divide=div, vars=kv)
 

@@ -215,15 +215,15 @@ def main():
         M = synth.config_matrix(cfg)
         print(f"# cfg{cfg} generated in {time.time() - t0:.1f} s", file=sys.stderr, flush=True)
         if cfg == 1:
-            run_spmv(1, M, "f64", [("A7", {}), ("A8", {}), ("A2", {}), ("A9", {})], args)
+            run_spmv(1, M, "f64", [("A7", {}), ("A8", {}), ("A2", {}), ("A9", {}), ("A1", {}), ("SPMV0", {})], args)
         elif cfg == 5:
-            run_spmv(5, M, "f64", [("A2", {}), ("A9", {}), ("A8", {}), ("A7", {})], args)
+            run_spmv(5, M, "f64", [("A2", {}), ("A9", {}), ("A8", {}), ("A7", {}), ("A1", {}), ("SPMV0", {})], args)
         elif cfg == 2:
             run_spmm(2, M, [("A4", {"NNZ_PER_TB": 4096, "NNZ_PER_WARP": 512}), ("K5", {})], args)
         elif cfg == 3:
             run_sddmm(3, M, [("K6", {"BOUND": 8}), ("K10", {})], args)
         elif cfg == 4:
-            run_csf(4, M, {"mttkrp": [("A6", {}), ("K9", {}), ("MTTKRP0", {})], "ttv": [("K7", {}), ("K11", {}),
+            run_csf(4, M, {"mttkrp": [("A6", {}), ("K9", {}), ("MTTKRP0", {}), ("A5", {})], "ttv": [("K7", {}), ("K11", {}),
                                 ("K11", {"NNZ_PER_TB": 4096, "NNZ_PER_WARP": 512, "NNZ_PER_THREAD": 16}),
                                 ("K11", {"NNZ_PER_TB": 8192, "NNZ_PER_WARP": 512, "NNZ_PER_THREAD": 16}),
                                 ("K11", {"NNZ_PER_TB": 2048, "NNZ_PER_WARP": 512, "NNZ_PER_THREAD": 16}),
