@@ -130,8 +130,8 @@ parallelize(thread, GPUThread, Atomics)""",
     Entry("A10", "PAPER.md:2059-2069 SpMM CPU tiled", SPMM, F_SPMM,
           """pos(j, jpos, A(i,j))
 split(jpos, jpos0, jpos1, {UNROLL_FACTOR})
-reorder(i, jpos0, k, jpos1)""", {"UNROLL_FACTOR": 8}, "spmm_row"),
-    Entry("A11", "PAPER.md:2071-2078 SpMM CPU untiled", SPMM, F_SPMM, "", {}, "spmm_row"),
+reorder(i, jpos0, k, jpos1)""", {"UNROLL_FACTOR": 8}, "spmm_nnz"),
+    Entry("A11", "PAPER.md:2071-2078 SpMM CPU untiled", SPMM, F_SPMM, "", {}, "spmm_nnz"),
     # -- GPU shapes beyond the appendix (SURVEY.md §8(a) row a20) --------
     Entry("K5", "warp-per-row SpMM (row a20 K5)", SPMM, F_SPMM,
           """split(i, block, block_row, {ROWS_PER_TB})
@@ -181,9 +181,16 @@ split(ipos, block, warp, {SLICES_PER_TB})
 reorder(block, warp, k, l, j)
 parallelize(block, GPUBlock, NoRaces)
 parallelize(warp, GPUWarp, NoRaces)""", {"SLICES_PER_TB": 8}, "mttkrp_slice"),
-    Entry("K10", "row-split SDDMM (unscheduled SDDMM shape)", SDDMM, F_SDDMM, "", {}, "sddmm_row"),
+    Entry("K10", "warp-per-row SDDMM (row a20 K10)", SDDMM, F_SDDMM,
+          """split(i, block, block_row, {ROWS_PER_TB})
+split(block_row, warp_row, warp, {WARPS_PER_TB})
+pos(j, jpos, B(i,j))
+reorder(block, warp, warp_row, jpos, k)
+parallelize(block, GPUBlock, NoRaces)
+parallelize(warp, GPUWarp, NoRaces)""", {"ROWS_PER_TB": 64, "WARPS_PER_TB": 8}, "sddmm_row"),
+    Entry("SDDMM0", "unscheduled SDDMM", SDDMM, F_SDDMM, "", {}, "sddmm_nnz"),
     Entry("TTV0", "unscheduled TTV", TTV, F_TTV, "", {}, "ttv_fiber"),
-    Entry("SPMV0", "unscheduled SpMV (Fig. 2b)", SPMV, F_SPMV, "", {}, "spmv_warp"),
+    Entry("SPMV0", "unscheduled SpMV (Fig. 2b)", SPMV, F_SPMV, "", {}, "spmv_nnz"),
     Entry("MTTKRP0", "unscheduled MTTKRP", MTTKRP, F_MTTKRP, "", {}, "mttkrp_slice"),
 ]
 

@@ -330,7 +330,9 @@ class ExecStats:
         loops: dict[str, int] = {}
         guards: dict[str, int] = {}
         kid = prog.kernel_id
-        if kid in (_lib.K_SPMV_NNZ, _lib.K_SPMM_NNZ, _lib.K_SDDMM_NNZ, _lib.K_MTTKRP_NNZ, _lib.K_TTV_NNZ):
+        if kid in (_lib.K_SPMV_NNZ, _lib.K_SPMM_NNZ, _lib.K_SDDMM_NNZ, _lib.K_MTTKRP_NNZ, _lib.K_TTV_NNZ) and not v:
+            pass  # an unscheduled statement on an nnz-split kernel: no parallel loops in the schedule
+        elif kid in (_lib.K_SPMV_NNZ, _lib.K_SPMM_NNZ, _lib.K_SDDMM_NNZ, _lib.K_MTTKRP_NNZ, _lib.K_TTV_NNZ):
             TB, W = p[0], p[1]
             blocks = _chunks(nnz, TB)
             warps = np.concatenate([_chunks(int(b), W) for b in blocks]) if len(blocks) else blocks

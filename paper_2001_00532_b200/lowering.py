@@ -414,6 +414,36 @@ def _check_tags(sh: _Shape, kernel_vars: dict, kernel: str) -> None:
             )
 
 
+def _serial(sh: _Shape) -> bool:
+    """A serial schedule: no parallel tag, no precompute and no MaxExact
+    bound -- the unscheduled loop nest (Fig. 2b) or one reshaped for a CPU
+    (A.10's unroll tiling).  It names no parallel instance whose work
+    ExecStats would report and no contract to check, so the GPU mapping is
+    the kernel's to choose."""
+    st = sh.stmt
+    return (not st.precomputes and all(st.tags_for(n).parallel_unit is None for n in sh.forest)
+            and not any(type(r).__name__ == "BoundRel" for r in st.provenance.rels))
+
+
+# serial SpMV / SpMM / SDDMM on CSR run on the nnz-split kernels with the
+# paper's constants and a deterministic output: SpMV's carry fix-up
+# (params[5] = 1), SpMM's owner store + ordered carry fix-up, SDDMM's
+# per-position store (no reduction) -- the row-split kernels' heaviest row
+# would otherwise set the time (cfg5 SpMV 9.1 ms thread per row, cfg2 SpMM
+# 6.2-6.6 ms and cfg3 SDDMM 5.4 ms warp per row)
+def _serial_nnz(sh: _Shape) -> Program | None:
+    ec = sh.ec
+    if not _serial(sh):
+        return None
+    if ec.kind == "spmv":
+        return Program(sh.stmt, ec, _lib.K_SPMV_NNZ, [2048, 256, 8, 0, 0, 1], vars={})
+    if ec.kind == "spmm":
+        return Program(sh.stmt, ec, _lib.K_SPMM_NNZ, [4096, 512, 0, 0], vars={})
+    if ec.kind == "sddmm":
+        return Program(sh.stmt, ec, _lib.K_SDDMM_NNZ, [2048, 256, 0, 0], vars={})
+    return None
+
+
 def _gpu_tagged(sh: _Shape) -> bool:
     """Does the schedule place any loop on a GPU unit?  CPU-tagged and
     unscheduled statements leave the GPU mapping to the kernel."""
@@ -622,7 +652,10 @@ def _lower_table(stmt, formats=None, dims=None) -> Program:
     ec = classify(stmt)
     sh = _Shape(stmt, ec)
     try:
-        if ec.kind == "spmv":
+        prog = _serial_nnz(sh)
+        if prog is not None:
+            pass
+        elif ec.kind == "spmv":
             prog = _match_spmv(sh)
         elif ec.kind == "spmm":
             prog = _match_spmm_like(sh, _lib.K_SPMM_NNZ, _lib.K_SPMM_ROW, "k", "pos[S](fuse(i,j))", ("j",))

@@ -27,7 +27,7 @@ T = _spindle.tensors
 KIND_ENTRIES = {
     "spmv": ["A1", "A2", "A7", "A8", "A9", "SPMV0"],
     "spmm": ["A3", "A4", "A10", "A11", "K5"],
-    "sddmm": ["K6", "K10"],
+    "sddmm": ["K6", "K10", "SDDMM0"],
     "ttv": ["K7", "K11", "TTV0"],
     "mttkrp": ["A5", "A6", "K9", "MTTKRP0"],
 }
