@@ -109,6 +109,29 @@ def main():
     assert np.array_equal(packed.to_dense().cpu().numpy(), T.pack(coo, T.parse_format("sds")).to_dense())
     assert packed.walk_stored().nnz == len(packed.vals)
     print("COO: ok", flush=True)
+    # serial schedules on the deterministic nnz-split kernels, and the K9
+    # heavy-slice cut (a 5,000-leaf slice > the 4,096-leaf range size)
+    for name in ("SPMV0", "SDDMM0", "MTTKRP0", "TTV0"):
+        e = corpus.BY_NAME[name]
+        prog = lower(corpus.build(name))
+        ins = _inputs(e, np.random.default_rng(4))
+        got, _ = interpret(prog, ins, sparse_output=False)
+        want = T.dense_eval(prog.stmt.assignment, ins).data
+        assert np.max(np.abs(got.data - want) / np.maximum(1.0, np.abs(want))) <= 1e-10, name
+    pos = {0: np.array([0, 2], np.int32), 1: np.array([0, 100, 103], np.int32),
+           2: np.concatenate([np.arange(0, 5001, 50), [5003, 5004, 5010]]).astype(np.int32)}
+    crd = {0: np.array([0, 3], np.int32), 1: np.concatenate([np.arange(100), [5, 7, 9]]).astype(np.int32),
+           2: np.concatenate([np.tile(np.arange(50), 100), [1, 2, 3, 4, 0, 1, 2, 3, 4, 5]]).astype(np.int32)}
+    vh = rng.uniform(-1, 1, 5010)
+    Ch, Dh = rng.uniform(-1, 1, (128, 32)), rng.uniform(-1, 1, (64, 32))
+    Bh = DeviceTensor.from_arrays((4, 128, 64), "sss", pos, crd, vh)
+    for name in ("A5", "K9"):
+        out = torch.empty(4 * 32, dtype=torch.float64, device="cuda")
+        Executor(lower(corpus.build(name)), {"B": Bh, "C": DeviceTensor.dense(Ch), "D": DeviceTensor.dense(Dh)},
+                 out, dtype="f64").launch()
+        want = O.mttkrp((4, 128, 64), pos, crd, vh, Ch, Dh)
+        assert np.max(np.abs(out.cpu().numpy().reshape(4, 32) - want)) <= 1e-9, name
+    print("serial schedules / K9 cut: ok", flush=True)
     print(f"all kernels ok; worst fp64 rel err {worst:.1e}")
 
 
