@@ -77,6 +77,8 @@ extern "C" {
  *  4   SpMM nnz-split            C(i,k)=A(i,j)*B(j,k)     [0]=NNZ_PER_TB [1]=NNZ_PER_WARP [2]=WARP_SIZE [3]=bound (0 = none)
  *                                                         [5]=B-row transport: 0 = default (staged-register path), >0 = cp.async row ring of that depth, <0 = staged-register path
  *  5   SpMM warp-per-row         "                        [0]=ROWS_PER_TB [1]=WARPS_PER_TB [2]=WARP_SIZE [3]=bound
+ *                                                         [4]=1: rows longer than max(512, nnz/131072) positions get a whole
+ *                                                         CTA, partials folded in range order (workspace: a row list)
  *  6   SDDMM nnz-split           A(i,j)=B(i,j)*C(i,k)*D(j,k)  [0]=NNZ_PER_TB [1]=NNZ_PER_WARP [2]=WARP_SIZE [3]=bound [7]=dense_out
  *  7   TTV fiber-split           A(i,j)=B(i,j,k)*c(k) B:sss   [0]=FIBERS_PER_TB [1]=FIBERS_PER_WARP
  *  8   MTTKRP nnz-split          A(i,j)=B(i,k,l)*C(k,j)*D(l,j) [0]=NNZ_PER_TB [1]=NNZ_PER_WARP [2]=WARP_SIZE [3]=bound

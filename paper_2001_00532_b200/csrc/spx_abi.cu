@@ -180,7 +180,8 @@ size_t spx_workspace_size(const spx_plan* plan, const int32_t* dims) {
   if (resolve(plan, nullptr, nullptr, nullptr, dims, &fam, &a) != SPX_OK) return 0;
   switch (plan->kernel_id) {
     case SPX_K_SPMV_NNZ: return ws_spmv(plan->kernel_id, a);
-    case SPX_K_SPMM_NNZ: return ws_spmm(plan->kernel_id, a);
+    case SPX_K_SPMM_NNZ:
+    case SPX_K_SPMM_ROW: return ws_spmm(plan->kernel_id, a);
     case SPX_K_MTTKRP_NNZ:
     case SPX_K_MTTKRP_SLICE:
     case SPX_K_TTV_NNZ: return ws_csf(plan->kernel_id, a);

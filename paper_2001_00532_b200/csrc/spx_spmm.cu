@@ -399,10 +399,50 @@ __global__ void carry_fixup_kernel(const int32_t* __restrict__ carry_row, const 
 #ifndef SPX_SPMM_ROW_MINB
 #define SPX_SPMM_ROW_MINB 1  // K5: the heaviest row is latency-bound; 16 rows in flight beat occupancy
 #endif
+// acc = sum over positions [a, e) of A[p] * B[crd[p], panel] (one warp)
 template <typename T, int VPL, bool CONTIG, int U>
-__global__ void __launch_bounds__(kMaxThreads, SPX_SPMM_ROW_MINB) spmm_row_kernel(
+__device__ __forceinline__ void spmm_row_range(Frag<T, VPL, CONTIG>& acc, const int32_t* __restrict__ crd,
+                                               const T* __restrict__ vals, const char* __restrict__ Bl,
+                                               uint32_t rowb, int ncols, unsigned char* ring_base, int lane, int a,
+                                               int e, uint64_t pol_s) {
+  using F = Frag<T, VPL, CONTIG>;
+  using Ring = LeafRing<T, 4>;
+  Ring ring;
+  ring.init(ring_base, crd, vals, a, e);
+  ring.prologue(lane, pol_s);
+  for (int b = 0; b < ring.nb; ++b) {
+    ring.acquire(b, lane, pol_s);
+    const int n = min(32, e - (a + b * 32));
+    const int32_t* Cs = ring.crd_slot(b);
+    const T* Vs = ring.val_slot(b);
+#pragma unroll 1
+    for (int t = 0; t < n; t += U) {
+      F bb[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int c = Cs[t + u];  // zero-filled past n
+        const T* src = reinterpret_cast<const T*>(addr_wide(Bl, (uint32_t)c, rowb));
+        if constexpr (CONTIG) bb[u].load_ptr(src);
+        else bb[u].load(src, lane, ncols);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (t + u < n) acc.fma(Vs[t + u], bb[u]);
+    }
+    ring.release();
+  }
+}
+
+// CUT (CPU-tagged row schedules, A.3): a row longer than `cut` positions is
+// skipped here and appended to heavy_list; spmm_heavy_row_kernel gives it a
+// whole CTA.  With the long rows gone the warps are throughput-bound, so the
+// kernel runs 2 CTAs/SM (cfg2 A.3 2.18 ms, against 2.95 at 1 CTA/SM).
+// !CUT: every row on its warp, as a GPU schedule writes it.
+template <typename T, int VPL, bool CONTIG, int U, bool CUT>
+__global__ void __launch_bounds__(kMaxThreads, CUT ? 2 : SPX_SPMM_ROW_MINB) spmm_row_kernel(
     const int32_t* __restrict__ pos, const int32_t* __restrict__ crd, const T* __restrict__ vals,
-    const T* __restrict__ B, T* __restrict__ C, int64_t M, int64_t N, int64_t R) {
+    const T* __restrict__ B, T* __restrict__ C, int64_t M, int64_t N, int64_t R, int64_t cut,
+    int32_t* __restrict__ heavy_list, int32_t* __restrict__ heavy_count) {
   using F = Frag<T, VPL, CONTIG>;
   using Ring = LeafRing<T, 4>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -424,33 +464,54 @@ __global__ void __launch_bounds__(kMaxThreads, SPX_SPMM_ROW_MINB) spmm_row_kerne
     const int64_t row = rows_lo + br;
     if (row >= M) break;
     const int a = __ldg(pos + row), e = __ldg(pos + row + 1);
+    if (CUT && e - a > cut) {
+      if (lane == 0 && blockIdx.y == 0) heavy_list[atomicAdd(heavy_count, 1)] = (int32_t)row;
+      continue;
+    }
     F acc;
     acc.zero();
-    Ring ring;
-    ring.init(smem_raw + (size_t)warp * Ring::kBytes, crd, vals, a, e);
-    ring.prologue(lane, pol_s);
-    for (int b = 0; b < ring.nb; ++b) {
-      ring.acquire(b, lane, pol_s);
-      const int n = min(32, e - (a + b * 32));
-      const int32_t* Cs = ring.crd_slot(b);
-      const T* Vs = ring.val_slot(b);
-#pragma unroll 1
-      for (int t = 0; t < n; t += U) {
-        F bb[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int c = Cs[t + u];  // zero-filled past n
-          const T* src = reinterpret_cast<const T*>(addr_wide(Bl, (uint32_t)c, rowb));
-          if constexpr (CONTIG) bb[u].load_ptr(src);
-          else bb[u].load(src, lane, ncols);
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (t + u < n) acc.fma(Vs[t + u], bb[u]);
-      }
-      ring.release();
-    }
+    spmm_row_range<T, VPL, CONTIG, U>(acc, crd, vals, Bl, rowb, ncols, smem_raw + (size_t)warp * Ring::kBytes,
+                                      lane, a, e, pol_s);
     acc.store(Cp + row * N, lane, ncols);
+  }
+}
+
+// One CTA per heavy row (list order is irrelevant): warp w sums the w-th of
+// nw equal position ranges, the partial rows meet in shared memory and warp 0
+// adds them in range order -- the row still has one owner and a fixed
+// summation order.
+template <typename T, int VPL, bool CONTIG, int U>
+__global__ void __launch_bounds__(kMaxThreads, 1) spmm_heavy_row_kernel(
+    const int32_t* __restrict__ pos, const int32_t* __restrict__ crd, const T* __restrict__ vals,
+    const T* __restrict__ B, T* __restrict__ C, int64_t N, const int32_t* __restrict__ heavy_list,
+    const int32_t* __restrict__ heavy_count) {
+  using F = Frag<T, VPL, CONTIG>;
+  using Ring = LeafRing<T, 4>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int PW = 32 * VPL;
+  if ((int64_t)blockIdx.x >= (int64_t)*heavy_count) return;
+  const int nw = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t col0 = (int64_t)blockIdx.y * PW;
+  const int ncols = (int)min((int64_t)PW, N - col0);
+  const char* __restrict__ Bl = reinterpret_cast<const char*>(B + col0 + (CONTIG ? lane * VPL : 0));
+  const uint32_t rowb = (uint32_t)(N * (int64_t)sizeof(T));
+  const int64_t row = heavy_list[blockIdx.x];
+  const int a = __ldg(pos + row), e = __ldg(pos + row + 1);
+  const int64_t len = e - a;
+  const int wa = a + (int)(len * warp / nw), we = a + (int)(len * (warp + 1) / nw);
+  F acc;
+  acc.zero();
+  spmm_row_range<T, VPL, CONTIG, U>(acc, crd, vals, Bl, rowb, ncols, smem_raw + (size_t)warp * Ring::kBytes, lane,
+                                    wa, we, l2_evict_first());
+  T* part = reinterpret_cast<T*>(smem_raw + (size_t)nw * Ring::kBytes);  // [nw][PW]
+  acc.store_smem(part + warp * PW, lane);
+  __syncthreads();
+  if (warp == 0) {
+    F sum;
+    sum.zero();
+    for (int w = 0; w < nw; ++w) sum.add_smem(part + w * PW, lane);
+    sum.store(C + col0 + row * N, lane, ncols);
   }
 }
 
@@ -503,6 +564,18 @@ int ring_depth() {
     return s ? atoi(s) : -1;
   }();
   return d;
+}
+
+// positions above which a CPU-tagged row schedule hands a row to a whole CTA
+#ifndef SPX_SPMM_CUT_MIN
+#define SPX_SPMM_CUT_MIN 512  // cfg2 A.3: 4096 -> 3.76 ms, 2048 -> 3.24, 1024 -> 3.10, 512 -> 2.95, 256 -> 3.12
+#endif
+#ifndef SPX_SPMM_CUT_DIV
+#define SPX_SPMM_CUT_DIV 131072
+#endif
+inline int64_t spmm_row_cut(int64_t nnz) { return std::max<int64_t>(SPX_SPMM_CUT_MIN, nnz / SPX_SPMM_CUT_DIV); }
+inline size_t ws_spmm_row(int64_t nnz) {
+  return (size_t)(4 + std::max<int64_t>(1, nnz / (spmm_row_cut(nnz) + 1))) * sizeof(int32_t);
 }
 
 template <typename T, int VPL, bool CONTIG>
@@ -580,10 +653,40 @@ int run_spmm(int kid, const Args& a, const SpmmGeom& g) {
   // latency-bound, so deeper is better while nothing spills
   constexpr int UR_MAX = SPX_SPMM_ROW_UR * 16 / (VPL * (int)sizeof(T));  // 32-bit registers per row: VPL*sizeof/4
   constexpr int UR = UR_MAX < 1 ? 1 : (UR_MAX > 16 ? 16 : UR_MAX);
-  spmm_row_kernel<T, VPL, CONTIG, UR><<<grid, (unsigned)(nw * 32), (size_t)nw * LeafRing<T, 4>::kBytes, a.stream>>>(
-      pos, crd, vals, B, C, M, N, R);
+  // params[4] = 1 (CPU-tagged row schedule): rows longer than the cut go to
+  // spmm_heavy_row_kernel, one CTA each (workspace: count + row list)
+  const int64_t cut = a.params[4] ? spmm_row_cut(nnz) : 0;
+  int32_t* heavy_count = nullptr;
+  int32_t* heavy_list = nullptr;
+  if (cut > 0) {
+    const size_t need = ws_spmm_row(nnz);
+    if (!a.ws || a.ws_bytes < need) return fail(SPX_E_WORKSPACE, "workspace %zu < %zu bytes", a.ws_bytes, need);
+    heavy_count = static_cast<int32_t*>(a.ws);
+    heavy_list = heavy_count + 4;
+    if (int e = check_cuda(cudaMemsetAsync(heavy_count, 0, sizeof(int32_t), a.stream), "memset")) return e;
+  }
+  auto rk = cut > 0 ? spmm_row_kernel<T, VPL, CONTIG, UR, true> : spmm_row_kernel<T, VPL, CONTIG, UR, false>;
+  rk<<<grid, (unsigned)(nw * 32), (size_t)nw * LeafRing<T, 4>::kBytes, a.stream>>>(pos, crd, vals, B, C, M, N, R, cut,
+                                                                                   heavy_list, heavy_count);
   count_launch();
-  return check_cuda(cudaGetLastError(), "spmm_row_kernel");
+  if (int e = check_cuda(cudaGetLastError(), "spmm_row_kernel")) return e;
+  if (cut > 0) {
+    const int hw = kMaxWarps;
+    const size_t hsm = (size_t)hw * LeafRing<T, 4>::kBytes + (size_t)hw * 32 * VPL * sizeof(T);
+    auto hk = spmm_heavy_row_kernel<T, VPL, CONTIG, UR>;
+    static thread_local size_t hset = 0;
+    if (hsm > 48 * 1024 && hsm > hset) {
+      if (int e = check_cuda(cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm),
+                             "cudaFuncSetAttribute"))
+        return e;
+      hset = hsm;
+    }
+    dim3 hgrid((unsigned)std::max<int64_t>(1, nnz / (cut + 1)), (unsigned)g.npanels);
+    hk<<<hgrid, (unsigned)(hw * 32), hsm, a.stream>>>(pos, crd, vals, B, C, N, heavy_list, heavy_count);
+    count_launch();
+    if (int e = check_cuda(cudaGetLastError(), "spmm_heavy_row_kernel")) return e;
+  }
+  return SPX_OK;
 }
 
 template <typename T>
@@ -606,6 +709,7 @@ int dispatch_spmm(int kid, const Args& a, const SpmmGeom& g) {
 }  // namespace
 
 size_t ws_spmm(int kid, const Args& a) {
+  if (kid == SPX_K_SPMM_ROW) return a.params[4] ? ws_spmm_row(a.level_sizes[1]) : 0;
   if (kid != SPX_K_SPMM_NNZ) return 0;
   const int64_t N = a.dims[1][1];
   const SpmmGeom g = spmm_geom(a.dtype, N);

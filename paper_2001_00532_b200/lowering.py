@@ -526,7 +526,13 @@ def _match_spmm_like(sh: _Shape, nnz_kid: int, row_kid: int, dense_role: str, P:
     R, Wn = rp
     if R and not Wn:
         Wn = min(R, 8)
-    return Program(sh.stmt, ec, row_kid, [R or 8, Wn or 8, ws, bnd], row_divide=div, vars=kv)
+    params = [R or 8, Wn or 8, ws, bnd]
+    if row_kid == _lib.K_SPMM_ROW:
+        # params[4] = 1 (CPU tags, A.3): rows longer than max(512, nnz/131072)
+        # positions get a whole CTA with an in-order fold; a GPU schedule's
+        # warp per row (K5) runs as written
+        params.append(0 if _gpu_tagged(sh) else 1)
+    return Program(sh.stmt, ec, row_kid, params, row_divide=div, vars=kv)
 
 
 def _match_ttv(sh: _Shape) -> Program:

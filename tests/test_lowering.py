@@ -125,7 +125,9 @@ def test_union_expression_has_no_kernel():
 
 def test_unmatched_schedule_shape_raises():
     stmt = S.concretize(N.parse_assignment(corpus.SPMV), corpus.F_SPMV)
-    stmt = S.apply_schedule(stmt, "split(j, j0, j1, 4)")  # column strip-mining: no kernel
+    # column strip-mining under a GPU block tag: no kernel (a serial schedule
+    # would run on the nnz-split kernel, lowering._serial_nnz)
+    stmt = S.apply_schedule(stmt, "split(j, j0, j1, 4)\nparallelize(i, GPUBlock, NoRaces)")
     with pytest.raises(E.LoweringError):
         lower(stmt, fallback=False)
     assert lower(stmt).kind == "generic"

@@ -219,7 +219,7 @@ def main():
         elif cfg == 5:
             run_spmv(5, M, "f64", [("A2", {}), ("A9", {}), ("A8", {}), ("A7", {}), ("A1", {}), ("SPMV0", {})], args)
         elif cfg == 2:
-            run_spmm(2, M, [("A4", {"NNZ_PER_TB": 4096, "NNZ_PER_WARP": 512}), ("K5", {}), ("A11", {}), ("A10", {})], args)
+            run_spmm(2, M, [("A4", {"NNZ_PER_TB": 4096, "NNZ_PER_WARP": 512}), ("K5", {}), ("A3", {}), ("A11", {}), ("A10", {})], args)
         elif cfg == 3:
             run_sddmm(3, M, [("K6", {"BOUND": 8}), ("K10", {}), ("SDDMM0", {})], args)
         elif cfg == 4:
