@@ -23,7 +23,8 @@ CASES = [
     ("a(i) = b(i) + c(i)", {"b": "s", "c": "s"}, None, ""),                   # union add
     ("A(i,j) = B(i,j) * C(i,j)", {"B": "ds", "C": "ds"}, None, ""),           # sparse x sparse (intersection)
     ("y(i) = A(i,j) * x(j)", {"A": "ss", "x": "d"}, None, ""),                # DCSR SpMV
-    ("y(i) = A(i,j) * x(j)", {"A": "ds", "x": "d"}, None, "split(j, j0, j1, 4)"),  # schedule outside the table
+    # a GPU schedule outside the table (serial ones run on the nnz-split kernels)
+    ("y(i) = A(i,j) * x(j)", {"A": "ds", "x": "d"}, None, "split(j, j0, j1, 4)\nparallelize(i, GPUBlock, NoRaces)"),
     ("C(i,k) = A(i,j) * B(j,k) + D(i,k)", {"A": "ds", "B": "dd", "D": "dd"}, None, ""),
     ("a(i) = B(i,j,k) * c(k) * d(j)", {"B": "sss", "c": "d", "d": "d"}, None, ""),
     ("A(i,j) = B(i,k,j) * c(k)", {"B": "dss", "c": "d"}, ["i", "k", "j"], ""),  # other mode order / formats
