@@ -88,6 +88,8 @@ extern "C" {
  *                                                         0: one warp per slice (a GPU schedule's warp-per-slice)
  *  10  SDDMM row-split           A(i,j)=B(i,j)*C(i,k)*D(j,k)  [0]=ROWS_PER_TB [1]=WARPS_PER_TB [2]=WARP_SIZE [3]=bound [7]=dense_out
  *  11  TTV nnz-split             A(i,j)=B(i,j,k)*c(k) B:sss   [0]=NNZ_PER_TB [1]=NNZ_PER_WARP [2]=NNZ_PER_THREAD
+ *                                                         [3]=1: fibers spanning warp chunks folded in chunk order
+ *                                                         (deterministic; workspace slots) instead of red.add
  *
  * Operand roles: the kernels address operands by role, and slot[role] gives
  * the role's index in the Manifest tensor order (vals[]/dims[] layout):

@@ -189,7 +189,7 @@ reorder(block, warp, warp_row, jpos, k)
 parallelize(block, GPUBlock, NoRaces)
 parallelize(warp, GPUWarp, NoRaces)""", {"ROWS_PER_TB": 64, "WARPS_PER_TB": 8}, "sddmm_row"),
     Entry("SDDMM0", "unscheduled SDDMM", SDDMM, F_SDDMM, "", {}, "sddmm_nnz"),
-    Entry("TTV0", "unscheduled TTV", TTV, F_TTV, "", {}, "ttv_fiber"),
+    Entry("TTV0", "unscheduled TTV", TTV, F_TTV, "", {}, "ttv_nnz"),
     Entry("SPMV0", "unscheduled SpMV (Fig. 2b)", SPMV, F_SPMV, "", {}, "spmv_nnz"),
     Entry("MTTKRP0", "unscheduled MTTKRP", MTTKRP, F_MTTKRP, "", {}, "mttkrp_slice"),
 ]

@@ -1260,12 +1260,18 @@ __device__ __forceinline__ int ld_i32_early(const int32_t* p) {
 #else
 #define SPX_TTV_BOUNDS __launch_bounds__(512)
 #endif
-template <typename T, int LPT, typename OffT>
+// DET (params[3] = 1, serial TTV): the lead and the open carry of a chunk go
+// to per-chunk slots that ttv_slot_fold_kernel adds in chunk order
+// (bit-identical repeats, cfg4 0.187 ms); !DET (K11 as scheduled, the
+// thread loop's Atomics): red.add into the zeroed A (0.177 ms).
+template <typename T, int LPT, typename OffT, bool DET>
 __global__ void SPX_TTV_BOUNDS ttv_stream_kernel(
     const int32_t* __restrict__ crd0, const int32_t* __restrict__ pos1, const int32_t* __restrict__ crd1,
     const int32_t* __restrict__ pos2, const int32_t* __restrict__ crd2, const T* __restrict__ vals,
     const T* __restrict__ c, const int32_t* __restrict__ chunkF, const int32_t* __restrict__ chunkS,
-    T* __restrict__ A, int S, int F, int nnz, int64_t J, int K, int nchunks, int csmem) {
+    T* __restrict__ A, int S, int F, int nnz, int64_t J, int K, int nchunks, int csmem,
+    int64_t* __restrict__ lead_off, T* __restrict__ lead_val, int64_t* __restrict__ carry_off,
+    T* __restrict__ carry_val) {
   static_assert(LPT % 4 == 0 && LPT <= 16, "rows of 4 or 8 leaves per lane");
   constexpr int CH = 32 * LPT;          // leaves per warp chunk
   constexpr int RL = LPT >= 8 ? 8 : 4;  // consecutive leaves per lane in a row
@@ -1361,6 +1367,8 @@ __global__ void SPX_TTV_BOUNDS ttv_stream_kernel(
     OffT open_off = off_in;  // fiber open at the end of the previous row
     bool started = false;    // has a fiber started in this chunk yet (warp-uniform)
     T carry = T(0);          // its partial so far in this chunk
+    int64_t my_lead_off = -1;  // the fiber open before the chunk, closed by my first start
+    T my_lead = T(0);
 #pragma unroll
     for (int h = 0; h < ROWS; ++h) {
       const unsigned hb = (hball >> (RL * h)) & RMASK;
@@ -1403,14 +1411,37 @@ __global__ void SPX_TTV_BOUNDS ttv_stream_kernel(
       T in = __shfl_up_sync(kFull, sv, 1);  // open partial arriving at my first leaf
       if (lane == 0) in = carry;
       if (seen) {  // my first start closes the fiber open before it
-        if (started || below) A[first_off] = in + lead;  // it started inside this chunk
-        else if (!(h == 0 && lane == 0 && lead_empty)) atomicAdd(A + first_off, in + lead);
+        if (started || below) {
+          A[first_off] = in + lead;  // it started inside this chunk
+        } else if (!(h == 0 && lane == 0 && lead_empty)) {
+          if constexpr (DET) {
+            my_lead_off = (int64_t)first_off;  // it started before: the chunk's lead slot
+            my_lead = in + lead;
+          } else {
+            atomicAdd(A + first_off, in + lead);
+          }
+        }
       }
       carry = __shfl_sync(kFull, sv, 31);
       open_off = __shfl_sync(kFull, cur, 31);
       started = started || rowheads != 0u;
     }
-    if (lane == 0) atomicAdd(A + open_off, carry);  // the fiber open at the chunk's end continues past it
+    // the lead (at most one lane) and the fiber open at the chunk's end go to
+    // the chunk's slots; ttv_slot_fold_kernel adds them in chunk order
+    if constexpr (DET) {
+      const unsigned lb = __ballot_sync(kFull, my_lead_off >= 0);
+      const int ls = lb ? __ffs(lb) - 1 : 0;
+      const int64_t lo = __shfl_sync(kFull, my_lead_off, ls);
+      const T lv = __shfl_sync(kFull, my_lead, ls);
+      if (lane == 0) {
+        lead_off[chunk] = lb ? lo : -1;
+        lead_val[chunk] = lv;
+        carry_off[chunk] = (int64_t)open_off;
+        carry_val[chunk] = carry;
+      }
+    } else if (lane == 0) {
+      atomicAdd(A + open_off, carry);  // the fiber open at the chunk's end continues past it
+    }
     fi = fi_n;
     si = si_n;
     __syncwarp();
@@ -1435,6 +1466,29 @@ TtvNnzLayout ttv_nnz_layout(const Args& a) {
 }
 
 
+// A fiber that spans chunks c..m: chunk c's open carry, the whole-chunk
+// carries of c+1..m-1 and chunk m's lead, added in chunk order by the thread
+// of the chunk where it starts (deterministic: the schedule's Atomics
+// strategy without atomics, like the SpMM carry fix-up).
+template <typename T>
+__global__ void ttv_slot_fold_kernel(const int64_t* __restrict__ lead_off, const T* __restrict__ lead_val,
+                                     const int64_t* __restrict__ carry_off, const T* __restrict__ carry_val,
+                                     int64_t nchunks, T* __restrict__ A) {
+  const int64_t ch = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (ch >= nchunks) return;
+  // a lead whose fiber starts exactly at this chunk's first leaf (it is no
+  // earlier chunk's carry) is the whole fiber
+  const int64_t lf = lead_off[ch];
+  if (lf >= 0 && (ch == 0 || carry_off[ch - 1] != lf)) A[lf] = lead_val[ch];
+  const int64_t f = carry_off[ch];
+  if (ch > 0 && carry_off[ch - 1] == f) return;  // started in an earlier chunk
+  T sum = carry_val[ch];
+  int64_t m = ch + 1;
+  for (; m < nchunks && carry_off[m] == f; ++m) sum += carry_val[m];
+  if (m < nchunks && lead_off[m] == f) sum += lead_val[m];
+  A[f] = sum;
+}
+
 template <typename T, int LPT, typename OffT>
 int launch_ttv_stream(const Args& a, const Csf& c, int64_t TB) {
   const int64_t I = a.dims[0][0], J = a.dims[0][1], K = a.dims[0][2];
@@ -1444,10 +1498,15 @@ int launch_ttv_stream(const Args& a, const Csf& c, int64_t TB) {
   const int csmem = (size_t)K * sizeof(T) <= 16384 ? 1 : 0;
   const size_t smem = (size_t)wpc * (CH * sizeof(OffT) + 128) + (csmem ? (size_t)K * sizeof(T) : 0);
   const int64_t nchunks = ceil_div(c.nnz, CH);
-  const size_t need = (size_t)2 * nchunks * sizeof(int32_t);
+  const size_t tab = ((size_t)2 * nchunks * sizeof(int32_t) + 255) & ~(size_t)255;
+  const size_t need = tab + (size_t)nchunks * 2 * (sizeof(int64_t) + sizeof(T));
   if (!a.ws || a.ws_bytes < need) return fail(SPX_E_WORKSPACE, "workspace %zu < %zu bytes", a.ws_bytes, need);
   int32_t* chunkF = static_cast<int32_t*>(a.ws);
   int32_t* chunkS = chunkF + nchunks;
+  int64_t* lead_off = reinterpret_cast<int64_t*>(static_cast<char*>(a.ws) + tab);
+  int64_t* carry_off = lead_off + nchunks;
+  T* lead_val = reinterpret_cast<T*>(carry_off + nchunks);
+  T* carry_val = lead_val + nchunks;
   T* A = static_cast<T*>(a.out);
   const int64_t nA = I * J;
   const int64_t prep_work = std::max<int64_t>(std::max<int64_t>(ceil_div(c.F, 8), nA * (int64_t)sizeof(T) / 16),
@@ -1457,13 +1516,14 @@ int launch_ttv_stream(const Args& a, const Csf& c, int64_t TB) {
                                                                  (int)c.F, CH);
   count_launch();
   if (int e = check_cuda(cudaGetLastError(), "ttv_prep_kernel")) return e;
-  auto kern = ttv_stream_kernel<T, LPT, OffT>;
-  static thread_local size_t attr_set = 0;
-  if (smem > 32 * 1024 && smem > attr_set) {
+  const bool det = a.params[3] != 0;
+  auto kern = det ? ttv_stream_kernel<T, LPT, OffT, true> : ttv_stream_kernel<T, LPT, OffT, false>;
+  static thread_local size_t attr_set[2] = {0, 0};  // per kernel variant (DET / atomics)
+  if (smem > 32 * 1024 && smem > attr_set[det]) {
     if (int e = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                            "smem attribute"))
       return e;
-    attr_set = smem;
+    attr_set[det] = smem;
   }
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
@@ -1471,9 +1531,15 @@ int launch_ttv_stream(const Args& a, const Csf& c, int64_t TB) {
   const int64_t grid = std::min<int64_t>((int64_t)num_sms() * per_sm, ceil_div(nchunks, wpc));
   kern<<<(unsigned)grid, (unsigned)threads, smem, a.stream>>>(
       c.crd0, c.pos1, c.crd1, c.pos2, c.crd2, static_cast<const T*>(a.vals[0]), static_cast<const T*>(a.vals[1]),
-      chunkF, chunkS, A, (int)c.S, (int)c.F, (int)c.nnz, J, (int)K, (int)nchunks, csmem);
+      chunkF, chunkS, A, (int)c.S, (int)c.F, (int)c.nnz, J, (int)K, (int)nchunks, csmem, lead_off, lead_val,
+      carry_off, carry_val);
   count_launch();
-  return check_cuda(cudaGetLastError(), "ttv_stream_kernel");
+  if (int e = check_cuda(cudaGetLastError(), "ttv_stream_kernel")) return e;
+  if (!det) return SPX_OK;
+  ttv_slot_fold_kernel<T><<<(unsigned)ceil_div(nchunks, 256), 256, 0, a.stream>>>(lead_off, lead_val, carry_off,
+                                                                                  carry_val, nchunks, A);
+  count_launch();
+  return check_cuda(cudaGetLastError(), "ttv_slot_fold_kernel");
 }
 
 template <typename T>
@@ -1527,8 +1593,11 @@ int run_ttv_nnz(const Args& a) {
 size_t ws_csf(int kid, const Args& a) {
   if (kid == SPX_K_TTV_NNZ) {
     const int tpt = a.params[2];
-    if (tpt == 4 || tpt == 8 || tpt == 16)  // the streaming form: the chunk table (fiber, slice)
-      return (size_t)2 * (size_t)ceil_div(a.level_sizes[2] > 0 ? a.level_sizes[2] : 1, 32 * tpt) * sizeof(int32_t);
+    if (tpt == 4 || tpt == 8 || tpt == 16) {  // the streaming form: chunk table (fiber, slice) + lead / carry slots
+      const size_t nch = (size_t)ceil_div(a.level_sizes[2] > 0 ? a.level_sizes[2] : 1, 32 * tpt);
+      const size_t es = a.dtype == SPX_F32 ? 4 : 8;
+      return ((2 * nch * sizeof(int32_t) + 255) & ~(size_t)255) + nch * 2 * (sizeof(int64_t) + es);
+    }
     return ttv_nnz_layout(a).total;
   }
   if (kid == SPX_K_MTTKRP_SLICE) {  // unit table + partial rows of split slices

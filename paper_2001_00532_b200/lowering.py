@@ -425,10 +425,10 @@ def _serial(sh: _Shape) -> bool:
             and not any(type(r).__name__ == "BoundRel" for r in st.provenance.rels))
 
 
-# serial SpMV / SpMM / SDDMM on CSR run on the nnz-split kernels with the
+# serial SpMV / SpMM / SDDMM / TTV run on the nnz-split kernels with the
 # paper's constants and a deterministic output: SpMV's carry fix-up
 # (params[5] = 1), SpMM's owner store + ordered carry fix-up, SDDMM's
-# per-position store (no reduction) -- the row-split kernels' heaviest row
+# per-position store (no reduction), TTV's chunk-ordered lead/carry fold -- the row-split kernels' heaviest row
 # would otherwise set the time (cfg5 SpMV 9.1 ms thread per row, cfg2 SpMM
 # 6.2-6.6 ms and cfg3 SDDMM 5.4 ms warp per row)
 def _serial_nnz(sh: _Shape) -> Program | None:
@@ -441,6 +441,8 @@ def _serial_nnz(sh: _Shape) -> Program | None:
         return Program(sh.stmt, ec, _lib.K_SPMM_NNZ, [4096, 512, 0, 0], vars={})
     if ec.kind == "sddmm":
         return Program(sh.stmt, ec, _lib.K_SDDMM_NNZ, [2048, 256, 0, 0], vars={})
+    if ec.kind == "ttv":  # the streaming K11, fibers spanning chunks folded in chunk order
+        return Program(sh.stmt, ec, _lib.K_TTV_NNZ, [8192, 512, 16, 1], vars={})
     return None
 
 

@@ -67,3 +67,25 @@ def test_serial_sddmm(cuda, rmat):
     got = _twice(prog, {"B": Bt, "C": DeviceTensor.dense(C, device=cuda), "D": DeviceTensor.dense(D, device=cuda)},
                  len(rmat.vals), "f64", cuda)
     assert rel_err(got, O.sddmm(rmat.pos, rmat.crd, rmat.vals, C, D)) <= 1e-10
+
+
+def test_serial_ttv_deterministic(cuda):
+    """TTV0 runs the streaming K11 kernel with params[3] = 1: fibers spanning
+    several warp chunks (3,000 and 2,048 leaves against 512-leaf chunks) are
+    folded in chunk order, so repeats are bit-identical.  K11 as scheduled
+    (red.add) gives the same values within fp32 rounding."""
+    from test_gpu_ttv_stream import _csf
+
+    dims, pos, crd, vals = _csf([3, 40], [3000, 2048, 700] + [30] * 40, 77)
+    c = np.random.default_rng(9).uniform(-1, 1, dims[2]).astype(np.float32)
+    v = vals.astype(np.float32)
+    want = O.ttv(dims, pos, crd, v, c)
+    B = DeviceTensor.from_arrays(dims, "sss", pos, crd, v, device=cuda, dtype="f32")
+    ops = {"B": B, "c": DeviceTensor.dense(c, device=cuda, dtype="f32")}
+    prog = lower(corpus.build("TTV0"))
+    assert prog.kernel == "ttv_nnz" and prog.params[3] == 1
+    got = _twice(prog, ops, dims[0] * dims[1], "f32", cuda)
+    assert rel_err(got.reshape(dims[0], dims[1]), want) <= 1e-4
+    out = torch.empty(dims[0] * dims[1], dtype=torch.float32, device=cuda)
+    Executor(lower(corpus.build("K11")), ops, out, dtype="f32").launch()
+    assert rel_err(out.cpu().numpy().reshape(dims[0], dims[1]), want) <= 1e-4

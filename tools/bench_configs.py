@@ -223,7 +223,7 @@ def main():
         elif cfg == 3:
             run_sddmm(3, M, [("K6", {"BOUND": 8}), ("K10", {}), ("SDDMM0", {})], args)
         elif cfg == 4:
-            run_csf(4, M, {"mttkrp": [("A6", {}), ("K9", {}), ("MTTKRP0", {}), ("A5", {})], "ttv": [("K7", {}), ("K11", {}),
+            run_csf(4, M, {"mttkrp": [("A6", {}), ("K9", {}), ("MTTKRP0", {}), ("A5", {})], "ttv": [("K7", {}), ("K11", {}), ("TTV0", {}),
                                 ("K11", {"NNZ_PER_TB": 4096, "NNZ_PER_WARP": 512, "NNZ_PER_THREAD": 16}),
                                 ("K11", {"NNZ_PER_TB": 8192, "NNZ_PER_WARP": 512, "NNZ_PER_THREAD": 16}),
                                 ("K11", {"NNZ_PER_TB": 2048, "NNZ_PER_WARP": 512, "NNZ_PER_THREAD": 16}),
