@@ -180,7 +180,7 @@ def test_partition_device_matches_host(cuda):
 
 @pytest.mark.parametrize("name", list(MATS))
 @pytest.mark.parametrize("sched,params", [("A7", {"ROWS_PER_TB": 64}), ("A8", {"ROWS_PER_TB": 16, "WARPS_PER_TB": 4}),
-                                          ("A1", {"CHUNK_SIZE": 5})])
+                                          ("A1", {"CHUNK_SIZE": 5}), ("SPMV0", {})])
 def test_spmv_row_schedules_edges(cuda, name, sched, params):
     pos, crd, vals, K = MATS[name]
     M = len(pos) - 1
@@ -214,15 +214,38 @@ def test_spmm_row_schedule_edges(cuda, name, N, dtype):
 
 
 @pytest.mark.parametrize("name", list(MATS))
+@pytest.mark.parametrize("sched", ["A3", "A10", "A11"])
+@pytest.mark.parametrize("N,dtype", [(128, np.float32), (40, np.float32), (64, np.float64)])
+def test_spmm_cpu_and_serial_schedule_edges(cuda, name, sched, N, dtype):
+    """A.3 (rows past the cut go to the heavy-row CTAs: one_long_row, single_row,
+    powerlaw) and the serial A.10 / A.11 (nnz-split, deterministic carries):
+    every row written, empty ones zero."""
+    pos, crd, vals, K = MATS[name]
+    M = len(pos) - 1
+    B = np.random.default_rng(6).uniform(-1, 1, (K, N)).astype(dtype)
+    v = vals.astype(dtype)
+    dt = "f32" if dtype == np.float32 else "f64"
+    prog = lower(corpus.build(sched))
+    ops = {"A": DeviceTensor.from_arrays((M, K), "ds", {1: pos}, {1: crd}, v, device=cuda, dtype=dt),
+           "B": DeviceTensor.dense(B, device=cuda, dtype=dt)}
+    out = torch.full((M * N,), float("nan"), dtype=torch.float32 if dt == "f32" else torch.float64, device=cuda)
+    Executor(prog, ops, out, dtype=dt).launch()
+    got = out.cpu().numpy().reshape(M, N)
+    assert not np.isnan(got).any()
+    assert rel_err(got, O.spmm(pos, crd, v, B)) <= (1e-4 if dt == "f32" else 1e-12)
+
+
+@pytest.mark.parametrize("name", list(MATS))
 @pytest.mark.parametrize("Kd", [256, 33])
-def test_sddmm_row_schedule_edges(cuda, name, Kd):
+@pytest.mark.parametrize("sched", ["K10", "SDDMM0"])
+def test_sddmm_row_schedule_edges(cuda, name, Kd, sched):
     pos, crd, vals, K = MATS[name]
     M = len(pos) - 1
     rng = np.random.default_rng(8)
     Cm = rng.uniform(-1, 1, (M, Kd)).astype(np.float32)
     Dm = rng.uniform(-1, 1, (K, Kd)).astype(np.float32)
     v = vals.astype(np.float32)
-    prog = lower(corpus.build("K10"))
+    prog = lower(corpus.build(sched))
     ops = {"B": DeviceTensor.from_arrays((M, K), "ds", {1: pos}, {1: crd}, v, device=cuda, dtype="f32"),
            "C": DeviceTensor.dense(Cm, device=cuda), "D": DeviceTensor.dense(Dm, device=cuda)}
     if len(crd) == 0:
