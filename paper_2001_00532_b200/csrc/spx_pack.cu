@@ -60,60 +60,111 @@ __device__ __forceinline__ int64_t block_exclusive_scan(int64_t v, int64_t* s_wa
   return before + x - v;
 }
 
-__global__ void __launch_bounds__(kScanThreads) scan_tiles_kernel(const int64_t* __restrict__ in,
-                                                                  int64_t* __restrict__ out, int64_t n,
-                                                                  int64_t* __restrict__ tile_sums) {
+// Single-pass scan with decoupled look-back: tiles are taken in launch order
+// from a counter, each publishes its aggregate, then its inclusive prefix once
+// the predecessors' prefixes are known (status word = flag << 62 | value;
+// flag 1 = aggregate, 2 = inclusive).  One read and one write of the data,
+// against two of each for the recursive tile-sum scan (cfg2 pack: the 12.5M-entry
+// radix offsets x 4 passes plus the 50M-entry run and level flags).
+constexpr uint64_t kStAgg = 1ull << 62, kStIncl = 2ull << 62, kStMask = (1ull << 62) - 1;
+
+__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void __launch_bounds__(kScanThreads) scan_lookback_kernel(const int64_t* __restrict__ in,
+                                                                     int64_t* __restrict__ out, int64_t n,
+                                                                     unsigned long long* __restrict__ status,
+                                                                     unsigned int* __restrict__ tile_ctr) {
   __shared__ int64_t s_warp[32];
-  const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  __shared__ int64_t s_prefix;
+  __shared__ unsigned int s_tile;
+  __shared__ int64_t s_x[kScanTile];  // warp-striped <-> thread-blocked transpose
+  if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
+  __syncthreads();
+  const int64_t tile = s_tile;
+  const int wl = threadIdx.x & 31, wbase = (threadIdx.x >> 5) * 32 * kScanItems;
+  const int64_t gw = tile * kScanTile + wbase;  // this warp's 32 * kScanItems elements
+  // coalesced loads (element k*32 + lane of the warp's run), then each thread
+  // takes kScanItems consecutive elements from shared memory
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    const int64_t g = gw + k * 32 + wl;
+    s_x[wbase + k * 32 + wl] = g < n ? in[g] : 0;
+  }
+  __syncwarp();
   int64_t v[kScanItems];
   int64_t t = 0;
 #pragma unroll
   for (int k = 0; k < kScanItems; ++k) {
-    v[k] = base + k < n ? in[base + k] : 0;
+    v[k] = s_x[wbase + wl * kScanItems + k];
     t += v[k];
   }
   int64_t total;
   int64_t run = block_exclusive_scan(t, s_warp, total);
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    int64_t excl = 0;
+    if (tile == 0) {
+      if (lane == 0) st_release(status, kStIncl | (unsigned long long)total);
+    } else {
+      if (lane == 0) st_release(status + tile, kStAgg | (unsigned long long)total);
+      int64_t j = tile - 1;
+      while (true) {
+        const int64_t idx = j - lane;
+        unsigned long long st;
+        do {
+          st = idx >= 0 ? ld_acquire(status + idx) : kStIncl;
+        } while (__any_sync(kFull, (st >> 62) == 0));
+        const unsigned incl = __ballot_sync(kFull, (st >> 62) == 2);
+        const int stop = incl ? __ffs(incl) - 1 : 31;  // the nearest inclusive prefix ends the walk
+        int64_t x = lane <= stop ? (int64_t)(st & kStMask) : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
+        excl += x;
+        if (incl) break;
+        j -= 32;
+      }
+      if (lane == 0) st_release(status + tile, kStIncl | (unsigned long long)(excl + total));
+    }
+    if (lane == 0) s_prefix = excl;
+  }
+  __syncthreads();
+  run += s_prefix;
 #pragma unroll
   for (int k = 0; k < kScanItems; ++k) {
-    if (base + k < n) out[base + k] = run;
+    s_x[wbase + wl * kScanItems + k] = run;
     run += v[k];
   }
-  if (threadIdx.x == 0 && tile_sums) tile_sums[blockIdx.x] = total;
-}
-
-__global__ void add_tile_offsets_kernel(int64_t* __restrict__ out, int64_t n, const int64_t* __restrict__ offs) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) out[i] += offs[i / kScanTile];
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    const int64_t g = gw + k * 32 + wl;
+    if (g < n) out[g] = s_x[wbase + k * 32 + wl];
+  }
 }
 
 size_t scan_ws_bytes(int64_t n) {
-  size_t b = 0;
-  while (n > kScanTile) {
-    n = ceil_div(n, kScanTile);
-    b += (size_t)n * 2 * sizeof(int64_t);
-  }
-  return b + 256;
+  const int64_t tiles = ceil_div(n > 0 ? n : 1, kScanTile);
+  return (size_t)(tiles + 1) * sizeof(unsigned long long) + 256;
 }
 
-// out[i] = sum(in[0..i)) ; returns SPX status.  ws holds the recursion.
+// out[i] = sum(in[0..i)) ; returns SPX status.  ws holds the tile status words
+// and the tile counter.
 int exclusive_scan(const int64_t* in, int64_t* out, int64_t n, int64_t* ws, cudaStream_t s) {
   if (n <= 0) return SPX_OK;
   const int64_t tiles = ceil_div(n, kScanTile);
-  if (tiles == 1) {
-    scan_tiles_kernel<<<1, kScanThreads, 0, s>>>(in, out, n, nullptr);
-    count_launch();
-    return check_cuda(cudaGetLastError(), "scan_tiles_kernel");
-  }
-  int64_t* sums = ws;
-  int64_t* sums_scanned = ws + tiles;
-  scan_tiles_kernel<<<(unsigned)tiles, kScanThreads, 0, s>>>(in, out, n, sums);
+  unsigned long long* status = reinterpret_cast<unsigned long long*>(ws);
+  unsigned int* ctr = reinterpret_cast<unsigned int*>(status + tiles);
+  if (int e = check_cuda(cudaMemsetAsync(ws, 0, (size_t)tiles * 8 + 8, s), "memset")) return e;
+  scan_lookback_kernel<<<(unsigned)tiles, kScanThreads, 0, s>>>(in, out, n, status, ctr);
   count_launch();
-  if (int e = check_cuda(cudaGetLastError(), "scan_tiles_kernel")) return e;
-  if (int e = exclusive_scan(sums, sums_scanned, tiles, ws + 2 * tiles, s)) return e;
-  add_tile_offsets_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(out, n, sums_scanned);
-  count_launch();
-  return check_cuda(cudaGetLastError(), "add_tile_offsets_kernel");
+  return check_cuda(cudaGetLastError(), "scan_lookback_kernel");
 }
 
 // ---------------------------------------------------------------------------
