@@ -428,9 +428,11 @@ def _serial(sh: _Shape) -> bool:
 # serial SpMV / SpMM / SDDMM / TTV run on the nnz-split kernels with the
 # paper's constants and a deterministic output: SpMV's carry fix-up
 # (params[5] = 1), SpMM's owner store + ordered carry fix-up, SDDMM's
-# per-position store (no reduction), TTV's chunk-ordered lead/carry fold -- the row-split kernels' heaviest row
-# would otherwise set the time (cfg5 SpMV 9.1 ms thread per row, cfg2 SpMM
-# 6.2-6.6 ms and cfg3 SDDMM 5.4 ms warp per row)
+# per-position store (no reduction), TTV's chunk-ordered lead/carry fold
+# (params[3] = 1).  The row-split kernels' heaviest row would otherwise set
+# the time (cfg5 SpMV 9.1 ms thread per row, cfg2 SpMM 6.2-6.6 ms and cfg3
+# SDDMM 5.4 ms warp per row, cfg4 TTV 0.35 ms fiber-split); serial MTTKRP
+# takes the cut slice-split (K9 params[2] = 1) in _match_mttkrp.
 def _serial_nnz(sh: _Shape) -> Program | None:
     ec = sh.ec
     if not _serial(sh):
@@ -492,10 +494,10 @@ def _match_spmv(sh: _Shape) -> Program:
     if len(jg) != 1 or next(iter(jg.values())).path != ():
         raise _NoMatch
     if not _gpu_tagged(sh):
-        # A.1 (CPU tags) and the unscheduled loop nest (Fig. 2b) name no GPU
-        # unit: each row keeps one owner, but the owner is a warp (K2, lanes
-        # over the row's positions, a fixed shuffle fold) rather than a thread
-        # -- cfg5: 1.73 ms against 9.2 ms thread per row
+        # A.1 (CPU tags) names no GPU unit: each row keeps one owner, but the
+        # owner is a warp (K2, lanes over the row's positions, a fixed
+        # shuffle fold) rather than a thread -- cfg5: 1.82 ms against 9.1 ms
+        # thread per row
         R = rp[0] or 8
         kv = {"block": rows.get("block"), "warp": rows.get("row", rows.get("warp"))}
         return Program(sh.stmt, ec, _lib.K_SPMV_WARP, [R, min(R, 8)], row_divide=div, vars=kv)
@@ -648,6 +650,19 @@ def lower(stmt, formats=None, dims=None, *, fallback: bool = True):
         return make_program(stmt, why=str(err), dims=dict(dims) if dims is not None else None)
 
 
+def _match(sh: _Shape) -> Program:
+    """The kernel-table row for a scheduled statement's shape (_NoMatch if none)."""
+    if sh.ec.kind == "spmv":
+        return _match_spmv(sh)
+    if sh.ec.kind == "spmm":
+        return _match_spmm_like(sh, _lib.K_SPMM_NNZ, _lib.K_SPMM_ROW, "k", "pos[S](fuse(i,j))", ("j",))
+    if sh.ec.kind == "sddmm":
+        return _match_spmm_like(sh, _lib.K_SDDMM_NNZ, _lib.K_SDDMM_ROW, "k", "pos[S](fuse(i,j))", ("j",))
+    if sh.ec.kind == "ttv":
+        return _match_ttv(sh)
+    return _match_mttkrp(sh)
+
+
 def _lower_table(stmt, formats=None, dims=None) -> Program:
     E = _err()
     if formats is not None:
@@ -660,19 +675,7 @@ def _lower_table(stmt, formats=None, dims=None) -> Program:
     ec = classify(stmt)
     sh = _Shape(stmt, ec)
     try:
-        prog = _serial_nnz(sh)
-        if prog is not None:
-            pass
-        elif ec.kind == "spmv":
-            prog = _match_spmv(sh)
-        elif ec.kind == "spmm":
-            prog = _match_spmm_like(sh, _lib.K_SPMM_NNZ, _lib.K_SPMM_ROW, "k", "pos[S](fuse(i,j))", ("j",))
-        elif ec.kind == "sddmm":
-            prog = _match_spmm_like(sh, _lib.K_SDDMM_NNZ, _lib.K_SDDMM_ROW, "k", "pos[S](fuse(i,j))", ("j",))
-        elif ec.kind == "ttv":
-            prog = _match_ttv(sh)
-        else:
-            prog = _match_mttkrp(sh)
+        prog = _serial_nnz(sh) or _match(sh)
         _check_launchable(prog)
     except _NoMatch:
         raise E.LoweringError(
