@@ -59,7 +59,7 @@ SCHEDULES = [("A5", {"CHUNK_SIZE": 8}, 1), ("MTTKRP0", {}, 1), ("K9", {"SLICES_P
 
 @pytest.mark.parametrize("case", list(ALL))
 @pytest.mark.parametrize("name,params,split", SCHEDULES)
-@pytest.mark.parametrize("R,dtype", [(32, "f32"), (16, "f32"), (64, "f32"), (32, "f64")])
+@pytest.mark.parametrize("R,dtype", [(32, "f32"), (16, "f32"), (64, "f32"), (32, "f64"), (48, "f32"), (8, "f64"), (1, "f32")])
 def test_mttkrp_slice(cuda, case, name, params, split, R, dtype):
     dims, pos, crd, vals = ALL[case]
     npdt = np.float32 if dtype == "f32" else np.float64

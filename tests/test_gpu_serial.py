@@ -89,3 +89,20 @@ def test_serial_ttv_deterministic(cuda):
     out = torch.empty(dims[0] * dims[1], dtype=torch.float32, device=cuda)
     Executor(lower(corpus.build("K11")), ops, out, dtype="f32").launch()
     assert rel_err(out.cpu().numpy().reshape(dims[0], dims[1]), want) <= 1e-4
+
+
+@pytest.mark.parametrize("lens", [[], [1], [1, 1, 1], [513], [512, 1, 511, 2]])
+def test_serial_ttv_small(cuda, lens):
+    """TTV0's ordered fold on the empty tensor, single leaves and fibers at the
+    512-leaf chunk boundary (fp64, against the oracle)."""
+    from test_gpu_ttv_stream import CASES, _csf
+
+    dims, pos, crd, vals = CASES["empty"] if not lens else _csf([len(lens)], lens, 5)
+    c = np.random.default_rng(2).uniform(-1, 1, dims[2])
+    B = DeviceTensor.from_arrays(dims, "sss", pos, crd, vals, device=cuda)
+    prog = lower(corpus.build("TTV0"))
+    out = torch.full((dims[0] * dims[1],), float("nan"), dtype=torch.float64, device=cuda)
+    Executor(prog, {"B": B, "c": DeviceTensor.dense(c, device=cuda)}, out, dtype="f64").launch()
+    got = out.cpu().numpy().reshape(dims[0], dims[1])
+    assert not np.isnan(got).any()
+    assert rel_err(got, O.ttv(dims, pos, crd, vals, c)) <= 1e-12

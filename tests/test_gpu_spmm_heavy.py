@@ -47,7 +47,7 @@ def _run(name, B, dtype, cuda):
     return prog, out.cpu().numpy().reshape(M, N), v
 
 
-@pytest.mark.parametrize("N", [128, 40, 300])
+@pytest.mark.parametrize("N", [128, 40, 300, 1])
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
 def test_spmm_heavy_rows(cuda, N, dtype):
     B = np.random.default_rng(N).uniform(-1, 1, (NCOL, N)).astype(np.float32 if dtype == "f32" else np.float64)
