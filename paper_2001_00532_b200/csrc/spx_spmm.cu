@@ -480,12 +480,18 @@ __global__ void __launch_bounds__(kMaxThreads, CUT ? 2 : SPX_SPMM_ROW_MINB) spmm
 // nw equal position ranges, the partial rows meet in shared memory and warp 0
 // adds them in range order -- the row still has one owner and a fixed
 // summation order.
-// 16 warps at 1 CTA/SM: the longest rows are latency-bound, so registers
-// for 16 B rows in flight beat occupancy (cfg2 A.3: 2.18 ms; 2 CTAs/SM at 64
-// registers 2.93 ms, 8 / 4 warps per row 4.20 / 7.05 ms -- tools/gpu_r02_ae.sh)
+// 16 warps per heavy row, 2 CTAs/SM with half the row kernel's B rows in
+// flight (tools/gpu_r02_az.sh); 8 / 4 warps per row were 4.20 / 7.05 ms
+// (tools/gpu_r02_ae.sh)
 constexpr int kHeavyWarps = 16;
+#ifndef SPX_SPMM_HEAVY_MINB
+#define SPX_SPMM_HEAVY_MINB 2  // cfg2 A.3: 2 CTAs/SM with 8 rows in flight 2.06 ms; 1 CTA/SM with 16: 2.15
+#endif
+#ifndef SPX_SPMM_HEAVY_UDIV
+#define SPX_SPMM_HEAVY_UDIV 2  // B rows in flight per warp: the row kernel's UR / this (/4: 2.36 ms)
+#endif
 template <typename T, int VPL, bool CONTIG, int U>
-__global__ void __launch_bounds__(kHeavyWarps * 32, 1) spmm_heavy_row_kernel(
+__global__ void __launch_bounds__(kHeavyWarps * 32, SPX_SPMM_HEAVY_MINB) spmm_heavy_row_kernel(
     const int32_t* __restrict__ pos, const int32_t* __restrict__ crd, const T* __restrict__ vals,
     const T* __restrict__ B, T* __restrict__ C, int64_t N, const int32_t* __restrict__ heavy_list,
     const int32_t* __restrict__ heavy_count) {
@@ -677,7 +683,7 @@ int run_spmm(int kid, const Args& a, const SpmmGeom& g) {
   if (cut > 0) {
     const int hw = kHeavyWarps;
     const size_t hsm = (size_t)hw * LeafRing<T, 4>::kBytes + (size_t)hw * 32 * VPL * sizeof(T);
-    auto hk = spmm_heavy_row_kernel<T, VPL, CONTIG, UR>;
+    auto hk = spmm_heavy_row_kernel<T, VPL, CONTIG, (UR / SPX_SPMM_HEAVY_UDIV > 0 ? UR / SPX_SPMM_HEAVY_UDIV : 1)>;
     static thread_local size_t hset = 0;
     if (hsm > 48 * 1024 && hsm > hset) {
       if (int e = check_cuda(cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm),
