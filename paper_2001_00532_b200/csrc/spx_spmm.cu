@@ -436,10 +436,16 @@ __device__ __forceinline__ void spmm_row_range(Frag<T, VPL, CONTIG>& acc, const 
 // CUT (CPU-tagged row schedules, A.3): a row longer than `cut` positions is
 // skipped here and appended to heavy_list; spmm_heavy_row_kernel gives it a
 // whole CTA.  With the long rows gone the warps are throughput-bound, so the
-// kernel runs 2 CTAs/SM (cfg2 A.3 2.18 ms, against 2.95 at 1 CTA/SM).
+// kernel trades rows in flight for occupancy (SPX_SPMM_CUT_MINB / _UDIV).
 // !CUT: every row on its warp, as a GPU schedule writes it.
+#ifndef SPX_SPMM_CUT_MINB
+#define SPX_SPMM_CUT_MINB 3  // cfg2 A.3: 3 CTAs/SM with 8 rows in flight 1.92 ms; 2 with 16: 2.07; 4 with 8: 2.02
+#endif
+#ifndef SPX_SPMM_CUT_UDIV
+#define SPX_SPMM_CUT_UDIV 2  // B rows in flight per warp in the cut row kernel: UR / this
+#endif
 template <typename T, int VPL, bool CONTIG, int U, bool CUT>
-__global__ void __launch_bounds__(kMaxThreads, CUT ? 2 : SPX_SPMM_ROW_MINB) spmm_row_kernel(
+__global__ void __launch_bounds__(kMaxThreads, CUT ? SPX_SPMM_CUT_MINB : SPX_SPMM_ROW_MINB) spmm_row_kernel(
     const int32_t* __restrict__ pos, const int32_t* __restrict__ crd, const T* __restrict__ vals,
     const T* __restrict__ B, T* __restrict__ C, int64_t M, int64_t N, int64_t R, int64_t cut,
     int32_t* __restrict__ heavy_list, int32_t* __restrict__ heavy_count) {
@@ -675,7 +681,8 @@ int run_spmm(int kid, const Args& a, const SpmmGeom& g) {
     heavy_list = heavy_count + 4;
     if (int e = check_cuda(cudaMemsetAsync(heavy_count, 0, sizeof(int32_t), a.stream), "memset")) return e;
   }
-  auto rk = cut > 0 ? spmm_row_kernel<T, VPL, CONTIG, UR, true> : spmm_row_kernel<T, VPL, CONTIG, UR, false>;
+  constexpr int URC = UR / SPX_SPMM_CUT_UDIV > 0 ? UR / SPX_SPMM_CUT_UDIV : 1;
+  auto rk = cut > 0 ? spmm_row_kernel<T, VPL, CONTIG, URC, true> : spmm_row_kernel<T, VPL, CONTIG, UR, false>;
   rk<<<grid, (unsigned)(nw * 32), (size_t)nw * LeafRing<T, 4>::kBytes, a.stream>>>(pos, crd, vals, B, C, M, N, R, cut,
                                                                                    heavy_list, heavy_count);
   count_launch();
