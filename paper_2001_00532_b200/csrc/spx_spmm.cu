@@ -396,11 +396,14 @@ __global__ void carry_fixup_kernel(const int32_t* __restrict__ carry_row, const 
 // broadcasts; B rows are gathered U at a time into registers.  A row longer
 // than the ring keeps streaming, so one warp on a long row still has ~U rows
 // of B and three batches of A in flight.
+#ifndef SPX_SPMM_ROW_PF
+#define SPX_SPMM_ROW_PF 1  // next-batch L1 prefetch of B rows in K5's row walk (cfg2 K5 6.21 -> 5.30 ms)
+#endif
 #ifndef SPX_SPMM_ROW_MINB
 #define SPX_SPMM_ROW_MINB 1  // K5: the heaviest row is latency-bound; 16 rows in flight beat occupancy
 #endif
 // acc = sum over positions [a, e) of A[p] * B[crd[p], panel] (one warp)
-template <typename T, int VPL, bool CONTIG, int U>
+template <typename T, int VPL, bool CONTIG, int U, bool PF = false>
 __device__ __forceinline__ void spmm_row_range(Frag<T, VPL, CONTIG>& acc, const int32_t* __restrict__ crd,
                                                const T* __restrict__ vals, const char* __restrict__ Bl,
                                                uint32_t rowb, int ncols, unsigned char* ring_base, int lane, int a,
@@ -411,7 +414,23 @@ __device__ __forceinline__ void spmm_row_range(Frag<T, VPL, CONTIG>& acc, const 
   ring.init(ring_base, crd, vals, a, e);
   ring.prologue(lane, pol_s);
   for (int b = 0; b < ring.nb; ++b) {
-    ring.acquire(b, lane, pol_s);
+    if constexpr (PF) {
+      // batches b and b+1 landed: batch b+1's B rows start moving into L1
+      // (each lane prefetches the lines of its leaf's row panel) -- a warp
+      // alone on a long row is latency-bound on these gathers
+      ring.issue(b + 3, lane, pol_s);
+      cp_async_wait<2>();
+      __syncwarp();
+      if (b + 1 < ring.nb && a + (b + 1) * 32 + lane < e) {
+        const char* rp = Bl - (CONTIG ? lane * VPL * (int)sizeof(T) : 0) +
+                         (size_t)(uint32_t)ring.crd_slot(b + 1)[lane] * rowb;
+#pragma unroll
+        for (int l = 0; l < (32 * VPL * (int)sizeof(T) + 127) / 128; ++l)
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(rp + l * 128));
+      }
+    } else {
+      ring.acquire(b, lane, pol_s);
+    }
     const int n = min(32, e - (a + b * 32));
     const int32_t* Cs = ring.crd_slot(b);
     const T* Vs = ring.val_slot(b);
@@ -476,8 +495,9 @@ __global__ void __launch_bounds__(kMaxThreads, CUT ? SPX_SPMM_CUT_MINB : SPX_SPM
     }
     F acc;
     acc.zero();
-    spmm_row_range<T, VPL, CONTIG, U>(acc, crd, vals, Bl, rowb, ncols, smem_raw + (size_t)warp * Ring::kBytes,
-                                      lane, a, e, pol_s);
+    spmm_row_range<T, VPL, CONTIG, U, !CUT && SPX_SPMM_ROW_PF>(acc, crd, vals, Bl, rowb, ncols,
+                                                               smem_raw + (size_t)warp * Ring::kBytes, lane, a, e,
+                                                               pol_s);
     acc.store(Cp + row * N, lane, ncols);
   }
 }
