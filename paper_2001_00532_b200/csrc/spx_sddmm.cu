@@ -23,6 +23,9 @@
 #ifndef SPX_SDDMM_ROW_UR
 #define SPX_SDDMM_ROW_UR 4   // cfg3 K10: 7.8 ms (2 rows, 2 CTAs/SM) -> 5.7 ms
 #endif
+#ifndef SPX_SDDMM_ROW_PF
+#define SPX_SDDMM_ROW_PF 1  // next-batch L1 prefetch of D rows in K10's row walk (cfg3 5.42 -> 4.67 ms)
+#endif
 #ifndef SPX_SDDMM_UN
 #define SPX_SDDMM_UN 2  // D rows (1 KB) in flight per warp; 4 spills at 64 registers (cfg3 1.68 vs 1.57 ms)
 #endif
@@ -187,7 +190,20 @@ __global__ void __launch_bounds__(kMaxThreads, SPX_SDDMM_ROW_MINB) sddmm_row_ker
     ring.init(smem_raw + (size_t)warp * Ring::kBytes, crd, vals, a, e);
     ring.prologue(lane, pol_s);
     for (int b = 0; b < ring.nb; ++b) {
+#if SPX_SDDMM_ROW_PF
+      // batches b and b+1 landed: batch b+1's D rows start moving into L1
+      // (a lane per leaf, one prefetch per 128 B line) -- the warp alone on
+      // the heaviest row is latency-bound on these gathers
+      ring.issue(b + 3, lane, pol_s);
+      cp_async_wait<2>();
+      __syncwarp();
+      if (b + 1 < ring.nb && a + (b + 1) * 32 + lane < e) {
+        const char* rp = reinterpret_cast<const char*>(Dm) + (size_t)(uint32_t)ring.crd_slot(b + 1)[lane] * rowb;
+        for (uint32_t l = 0; l < rowb; l += 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(rp + l));
+      }
+#else
       ring.acquire(b, lane, pol_s);
+#endif
       const int p = a + b * 32;
       const int n = min(32, e - p);
       const int32_t* Cs = ring.crd_slot(b);
