@@ -37,6 +37,9 @@ constexpr int kPosCache = 4096;  // ints of pos staged per CTA
 #ifndef SPX_SPMV_WARP_STEPS
 #define SPX_SPMV_WARP_STEPS 8  // cfg5 A8 2.29 -> 1.70 ms; 16 steps at 1 CTA/SM: 2.47
 #endif
+#ifndef SPX_SPMV_ROW_PF
+#define SPX_SPMV_ROW_PF 4  // L2 prefetch distance (steps) of the thread-per-row streams (cfg5 A.7 9.13 -> 8.02 ms; 16: 8.10)
+#endif
 #ifndef SPX_SPMV_WARP_MINB
 #define SPX_SPMV_WARP_MINB 2
 #endif
@@ -59,6 +62,16 @@ __global__ void __launch_bounds__(kMaxThreads, SPX_SPMV_ROW_MINB) spmv_row_kerne
     for (; p + STEP <= e; p += STEP) {
       int c[STEP];
       T v[STEP], xv[STEP];
+#if SPX_SPMV_ROW_PF
+      // a thread alone on a long row is a serial latency chain: pull the
+      // (crd, vals) lines SPX_SPMV_ROW_PF steps ahead into L2
+      if (p + (SPX_SPMV_ROW_PF + 1) * STEP <= e) {
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(crd + p + SPX_SPMV_ROW_PF * STEP));
+#pragma unroll
+        for (int l = 0; l < STEP * (int)sizeof(T); l += 128)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(vals + p + SPX_SPMV_ROW_PF * STEP) + l));
+      }
+#endif
 #pragma unroll
       for (int k = 0; k < STEP; ++k) {
         c[k] = __ldcs(crd + p + k);
